@@ -1,0 +1,541 @@
+// C ABI of the binpaths B200 engine (include/binpaths_b200.h).
+//
+// Host side of the drop-in boundary: validation with the reference's error
+// classes, layout selection, table construction, launches, multi-device
+// sharding with one host thread per GPU, and the fixed-order combination of
+// super-block partials.  Reference call sites: exact.py:75-133 (exact),
+// mc.py:92-100,197-213,287-331 (Monte Carlo).
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/binpaths_b200.h"
+#include "bp_exact.cuh"
+#include "bp_kernels.h"
+
+using namespace bp;
+
+// ---------------------------------------------------------------------------
+// error state
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define BP_CUDA(call)                                                                          \
+  do {                                                                                         \
+    cudaError_t e_ = (call);                                                                   \
+    if (e_ != cudaSuccess)                                                                     \
+      return fail(BP_E_CUDA, std::string("CUDA error ") + cudaGetErrorString(e_) + " at " +    \
+                                 __FILE__ + ":" + std::to_string(__LINE__) + " (" #call ")"); \
+  } while (0)
+
+extern "C" const char* bp_last_error(void) { return g_err.c_str(); }
+extern "C" int bp_abi_version(void) { return BP_ABI_VERSION; }
+
+extern "C" int bp_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+// ---------------------------------------------------------------------------
+// validation (mirrors model.py:62-76 / exact.py:48-56 domains that the
+// engine itself relies on; the Python mirror validates request objects
+// before calling, so these are a second line of defence)
+static int validate_tree(const bp_tree* t, int max_n) {
+  if (!t) return fail(BP_E_INVALID_INPUT, "tree is NULL");
+  if (t->n_steps < 1 || t->n_steps > max_n)
+    return fail(BP_E_INVALID_INPUT, "N must be between 1 and " + std::to_string(max_n) + ", got " +
+                                        std::to_string(t->n_steps));
+  if (!(t->S0 > 0.0) || !std::isfinite(t->S0))
+    return fail(BP_E_INVALID_INPUT, "S0 must be a positive finite number");
+  if (!std::isfinite(t->K)) return fail(BP_E_INVALID_INPUT, "K must be finite");
+  if (!(t->u > 0.0) || !std::isfinite(t->u) || !(t->d > 0.0) || !std::isfinite(t->d))
+    return fail(BP_E_INVALID_INPUT, "u and d must be positive finite numbers");
+  if (!std::isfinite(t->disc)) return fail(BP_E_INVALID_INPUT, "discount must be finite");
+  if (!t->up_probs) return fail(BP_E_LENGTH_MISMATCH, "up_probs is NULL");
+  for (int i = 0; i < t->n_steps; ++i) {
+    const double p = t->up_probs[i];
+    if (!(p >= 0.0 && p <= 1.0))
+      return fail(BP_E_PROBABILITY, "up probability " + std::to_string(p) + " is outside [0, 1]");
+  }
+  return BP_OK;
+}
+
+static int kinds_ok(uint32_t payoffs) {
+  if (payoffs == 0 || (payoffs >> BP_N_PAYOFFS) != 0)
+    return fail(BP_E_INVALID_INPUT, "payoff mask must be a non-empty OR of bp_payoff bits");
+  return BP_OK;
+}
+
+static bool constant_p(const bp_tree* t) {
+  for (int i = 1; i < t->n_steps; ++i)
+    if (t->up_probs[i] != t->up_probs[0]) return false;
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// layout: a pure function of (N, engine) so every device count and every
+// machine uses the same decomposition (bitwise reproducibility across G).
+static const int kFastL = 8;
+
+struct TableSet {
+  std::vector<double> t[3];  // c, mx, mn  (unscaled), 2^L
+  double scale_up[3], scale_dn[3];
+  bool ok[3];
+};
+
+static void build_inner(int L, double u, double d, std::vector<double>& c, std::vector<double>& mx,
+                        std::vector<double>& mn, std::vector<double>& e, std::vector<int>& h) {
+  const int n = 1 << L;
+  c.assign(n, 0.0);
+  mx.assign(n, 0.0);
+  mn.assign(n, 0.0);
+  e.assign(n, 1.0);
+  h.assign(n, 0);
+  for (int s = 0; s < n; ++s) {
+    double r = 1.0, cs = 0.0, m1 = 0.0, m2 = INFINITY;
+    int ups = 0;
+    for (int j = 0; j < L; ++j) {
+      const int b = (s >> (L - 1 - j)) & 1;
+      r *= b ? u : d;
+      cs += r;
+      m1 = std::max(m1, r);
+      m2 = std::min(m2, r);
+      ups += b;
+    }
+    c[s] = cs;
+    mx[s] = m1;
+    mn[s] = m2;
+    e[s] = r;
+    h[s] = ups;
+  }
+}
+
+// a = 1 - e where min = f 2^e, f in [0.5, 1): scaled min in [1, 2)
+static bool table_scale(const std::vector<double>& t, double& up, double& dn) {
+  double mn = INFINITY, mxv = 0.0;
+  for (double v : t) {
+    mn = std::min(mn, v);
+    mxv = std::max(mxv, v);
+  }
+  if (!(mn > 0.0) || !std::isfinite(mxv)) return false;
+  int e = 0;
+  std::frexp(mn, &e);
+  const int a = 1 - e;
+  if (a < -(1023 - kMaskExp) + 0 || a > 1000) return false;  // 2^(1007-a) must be finite
+  if (kMaskExp - a > 1023) return false;
+  up = std::ldexp(1.0, a);
+  dn = std::ldexp(1.0, kMaskExp - a);
+  if (!std::isfinite(mxv * up) || mxv * up > 1e300) return false;
+  return true;
+}
+
+static int ilog2_floor(unsigned long long x) { return 63 - __builtin_clzll(x); }
+
+static Layout choose_layout(const bp_tree* t, uint32_t payoffs, uint32_t flags, bool* fast_possible) {
+  const int N = t->n_steps;
+  Layout lay{};
+  bool fast = !(flags & BP_FLAG_GENERIC) && N >= kFastMinN && constant_p(t);
+  if (fast) {
+    const double p = t->up_probs[0];
+    if (!(p > 0.0 && p < 1.0)) fast = false;  // degenerate: single-path mass, walk it
+  }
+  if (fast) {
+    // every requested kind must have a fast kernel (each kind can be launched alone)
+    for (int k = 0; k < kNumKinds; ++k)
+      if (((payoffs >> k) & 1) && !fast_kind_mask_supported(1u << k)) fast = false;
+  }
+  if (fast) {
+    std::vector<double> c, mx, mn, e;
+    std::vector<int> h;
+    build_inner(kFastL, t->u, t->d, c, mx, mn, e, h);
+    double up, dn;
+    if (!table_scale(c, up, dn) || !table_scale(mx, up, dn) || !table_scale(mn, up, dn)) fast = false;
+  }
+  if (fast_possible) *fast_possible = fast;
+  if (fast) {
+    lay.engine = 1;
+    lay.L = kFastL;
+    lay.D = N - kFastL;
+    const int free_bits = lay.D - 5;  // bits above the lane
+    lay.m = std::max(0, std::min(6, free_bits - kUnitTargetLog2));
+    lay.Dp = lay.D - lay.m;
+    const int unit_bits = free_bits - lay.m;
+    lay.q = std::max(0, unit_bits - 18);
+    lay.units = 1ull << (unit_bits - lay.q);
+    lay.g = 0;
+  } else {
+    lay.engine = 0;
+    lay.L = 0;
+    lay.D = N;
+    const int free_bits = std::max(0, N - 5);
+    lay.g = std::max(0, free_bits - kUnitTargetLog2);
+    lay.units = 1ull << (free_bits - lay.g);
+    lay.m = lay.Dp = lay.q = 0;
+  }
+  lay.n_sb = (int)std::min<unsigned long long>(kMaxSB, lay.units);
+  lay.units_per_sb = lay.units / lay.n_sb;
+  return lay;
+}
+
+static int build_fast_args(const bp_tree* t, const Layout& lay, unsigned km, std::vector<unsigned char>& buf) {
+  const int L = lay.L;
+  if (L != 8) return fail(BP_E_INVALID_INPUT, "unsupported inner block size");
+  buf.assign(exact_args_size(L), 0);
+  ExactArgs<8>& a = *reinterpret_cast<ExactArgs<8>*>(buf.data());
+  std::vector<double> c, mx, mn, e;
+  std::vector<int> h;
+  build_inner(L, t->u, t->d, c, mx, mn, e, h);
+  const std::vector<double>* tabs[3] = {&c, &mx, &mn};
+  double up[3] = {1, 1, 1}, dn[3] = {1, 1, 1};
+  for (int i = 0; i < 3; ++i)
+    if (!table_scale(*tabs[i], up[i], dn[i])) return fail(BP_E_INVALID_INPUT, "lattice outside the fast engine range");
+  // slot assignment: slot 0 = first table in use, slot 1 = second
+  int slot = 0;
+  const bool useT[3] = {(km & ((1u << kAC) | (1u << kAP))) != 0, (km & (1u << kFL)) != 0, (km & (1u << kFLP)) != 0};
+  for (int ti = 0; ti < 3; ++ti) {
+    if (!useT[ti]) continue;
+    if (slot > 1) return fail(BP_E_INVALID_INPUT, "more than two inner tables requested in one launch");
+    for (int s = 0; s < (1 << L); ++s) a.tab[slot][s] = (*tabs[ti])[s] * up[ti];
+    ++slot;
+  }
+  // middle tables (chunk of m steps)
+  const int m = lay.m;
+  std::vector<double> mc, mmx, mmn, me;
+  std::vector<int> mh;
+  if (m > 0) {
+    build_inner(m, t->u, t->d, mc, mmx, mmn, me, mh);
+  } else {
+    mc = {0.0};
+    mmx = {0.0};
+    mmn = {INFINITY};
+    me = {1.0};
+    mh = {0};
+  }
+  for (int j = 0; j < (1 << m); ++j) {
+    a.mid_c[j] = mc[j];
+    a.mid_e[j] = me[j];
+    a.mid_mx[j] = mmx[j];
+    a.mid_mn[j] = mmn[j];
+    a.mid_h[j] = mh[j];
+  }
+  // weights, discount folded in (exact.py:95,99)
+  const int N = t->n_steps;
+  const double p = t->up_probs[0];
+  for (int k = 0; k <= N; ++k) a.w[k] = t->disc * std::pow(p, k) * std::pow(1.0 - p, N - k);
+  for (int k = N + 1; k < kMaxN + 2; ++k) a.w[k] = 0.0;
+  for (int cc = 0; cc <= L; ++cc) {
+    double r = 1.0;
+    for (int j = 0; j < cc; ++j) r *= t->u;
+    for (int j = cc; j < L; ++j) r *= t->d;
+    a.e_cls[cc] = r;
+    double b = 1.0;
+    for (int j = 0; j < cc; ++j) b = b * (L - j) / (j + 1);
+    a.b_cls[cc] = std::round(b);
+  }
+  ExactScalars& s = a.s;
+  s.S0 = t->S0;
+  s.K = t->K;
+  s.NK = (double)N * t->K;
+  s.u = t->u;
+  s.d = t->d;
+  s.invN = 1.0 / N;
+  for (int i = 0; i < 3; ++i) {
+    s.sc_up[i] = up[i];
+    s.sc_dn[i] = dn[i];
+  }
+  s.N = N;
+  s.L = L;
+  s.D = lay.D;
+  s.m = m;
+  s.Dp = lay.Dp;
+  s.n_mid = 1 << m;
+  s.q = lay.q;
+  s.zero = 0;
+  return BP_OK;
+}
+
+// the groups of kinds launched together in the fast engine
+static std::vector<unsigned> fast_groups(uint32_t payoffs) {
+  std::vector<unsigned> g;
+  unsigned rest = payoffs;
+  const unsigned pair = (1u << kAC) | (1u << kFL);
+  if ((rest & pair) == pair) {
+    g.push_back(pair);
+    rest &= ~pair;
+  }
+  for (int k = 0; k < kNumKinds; ++k)
+    if ((rest >> k) & 1) g.push_back(1u << k);
+  return g;
+}
+
+static int device_sm_count(int dev) {
+  int n = 0;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n > 0 ? n : 1;
+}
+
+// Enqueue the valuation of super-blocks [sb_first, sb_first+sb_count) on
+// the current device.  out_dev: [sb_count][6][2] doubles (device).
+static int enqueue_superblocks(const bp_tree* t, uint32_t payoffs, uint32_t flags, int dev, int sb_first,
+                               int sb_count, double* out_dev, unsigned long long* hist_dev, cudaStream_t st) {
+  const Layout lay = choose_layout(t, payoffs, flags, nullptr);
+  if (sb_first < 0 || sb_count < 1 || sb_first + sb_count > lay.n_sb)
+    return fail(BP_E_RANK_RANGE, "super-block range [" + std::to_string(sb_first) + ", " +
+                                     std::to_string(sb_first + sb_count) + ") outside [0, " +
+                                     std::to_string(lay.n_sb) + ")");
+  const bool cnt = (flags & BP_FLAG_COUNT) != 0;
+  if (cnt && !hist_dev) return fail(BP_E_INVALID_INPUT, "BP_FLAG_COUNT needs a histogram buffer");
+  const unsigned long long u0 = (unsigned long long)sb_first * lay.units_per_sb;
+  const unsigned long long u1 = u0 + (unsigned long long)sb_count * lay.units_per_sb;
+  const unsigned long long n_units = u1 - u0;
+  double2* unit_out = nullptr;
+  BP_CUDA(cudaMallocAsync((void**)&unit_out, sizeof(double2) * kNumKinds * n_units, st));
+  // kernels index unit_out by absolute unit; shift the base pointer
+  double2* unit_base = unit_out - (ptrdiff_t)(u0 * kNumKinds);
+  BP_CUDA(cudaMemsetAsync(out_dev, 0, sizeof(double) * 2 * kNumKinds * sb_count, st));
+  const int sms = device_sm_count(dev);
+  if (lay.engine == 1) {
+    bool first_group = true;  // bookkeeping once per valuation, not per kind group
+    for (unsigned km : fast_groups(payoffs)) {
+      const bool cnt_g = cnt && first_group;
+      first_group = false;
+      std::vector<unsigned char> buf;
+      int rc = build_fast_args(t, lay, km, buf);
+      if (rc) return rc;
+      ExactArgs<8>& a = *reinterpret_cast<ExactArgs<8>*>(buf.data());
+      a.s.unit_first = u0;
+      a.s.unit_end = u1;
+      const int occ = std::max(1, occupancy_exact_fast(lay.L, km, cnt_g));
+      const unsigned long long want = (n_units + 7) / 8;
+      const int grid = (int)std::max<unsigned long long>(1, std::min<unsigned long long>(want, (unsigned long long)occ * sms));
+      BP_CUDA(launch_exact_fast(lay.L, km, buf.data(), cnt_g, grid, st, unit_base, hist_dev));
+      BP_CUDA(launch_sb_reduce(unit_base, lay.units_per_sb, sb_first, sb_count, km, 1.0 / t->n_steps, out_dev, st));
+    }
+  } else {
+    GenericArgs g{};
+    g.S0 = t->S0;
+    g.K = t->K;
+    g.u = t->u;
+    g.d = t->d;
+    g.disc = t->disc;
+    g.invN = 1.0 / t->n_steps;
+    for (int i = 0; i < t->n_steps; ++i) g.p[i] = t->up_probs[i];
+    g.N = t->n_steps;
+    g.g = lay.g;
+    g.kinds = payoffs;
+    g.unit_first = u0;
+    g.unit_end = u1;
+    g.n_codes = 1ull << t->n_steps;
+    const int occ = std::max(1, occupancy_exact_generic(cnt));
+    const unsigned long long want = (n_units + 7) / 8;
+    const int grid = (int)std::max<unsigned long long>(1, std::min<unsigned long long>(want, (unsigned long long)occ * sms));
+    BP_CUDA(launch_exact_generic(g, cnt, grid, st, unit_base, hist_dev));
+    BP_CUDA(launch_sb_reduce(unit_base, lay.units_per_sb, sb_first, sb_count, payoffs, 1.0, out_dev, st));
+  }
+  BP_CUDA(cudaFreeAsync(unit_out, st));
+  return BP_OK;
+}
+
+extern "C" int bp_exact_layout(const bp_tree* tree, uint32_t payoffs, uint32_t flags, int* n_superblocks,
+                               int* engine, int* inner_bits) {
+  int rc = validate_tree(tree, 62);
+  if (rc) return rc;
+  if ((rc = kinds_ok(payoffs))) return rc;
+  const Layout lay = choose_layout(tree, payoffs, flags, nullptr);
+  if (n_superblocks) *n_superblocks = lay.n_sb;
+  if (engine) *engine = lay.engine;
+  if (inner_bits) *inner_bits = lay.L;
+  return BP_OK;
+}
+
+extern "C" int bp_exact_superblocks(const bp_tree* tree, uint32_t payoffs, uint32_t flags, int device, int sb_first,
+                                    int sb_count, double* out_dev, uint64_t* hist_dev, void* stream) {
+  int rc = validate_tree(tree, 62);
+  if (rc) return rc;
+  if ((rc = kinds_ok(payoffs))) return rc;
+  if (device < 0 || device >= bp_device_count()) return fail(BP_E_NO_DEVICE, "no CUDA device " + std::to_string(device));
+  BP_CUDA(cudaSetDevice(device));
+  return enqueue_superblocks(tree, payoffs, flags, device, sb_first, sb_count, out_dev,
+                             reinterpret_cast<unsigned long long*>(hist_dev), static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int bp_combine_superblocks(const double* partials, int n_sb, uint32_t payoffs, double* values) {
+  if (!partials || !values || n_sb < 1) return fail(BP_E_INVALID_INPUT, "bad combine arguments");
+  for (int k = 0; k < BP_N_PAYOFFS; ++k) {
+    double s = 0.0, c = 0.0;
+    if ((payoffs >> k) & 1)
+      for (int b = 0; b < n_sb; ++b) comp_merge(s, c, partials[(b * BP_N_PAYOFFS + k) * 2], partials[(b * BP_N_PAYOFFS + k) * 2 + 1]);
+    values[k] = s + c;
+  }
+  return BP_OK;
+}
+
+// one device's share of a synchronous valuation
+struct DeviceJob {
+  int device, sb_first, sb_count;
+  std::vector<double> partials;       // sb_count * 6 * 2
+  std::vector<unsigned long long> hist;  // 66
+  float ms = 0.f;
+  int rc = BP_OK;
+  std::string err;
+};
+
+static void run_device_job(const bp_tree* t, uint32_t payoffs, uint32_t flags, DeviceJob* job) {
+  auto setrc = [&](int rc) {
+    job->rc = rc;
+    job->err = g_err;
+  };
+  auto cuda_fail = [&](cudaError_t e, const char* what) {
+    job->rc = BP_E_CUDA;
+    job->err = std::string("CUDA error ") + cudaGetErrorString(e) + " (" + what + ")";
+  };
+  cudaError_t e = cudaSetDevice(job->device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  cudaStream_t st;
+  if ((e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)) != cudaSuccess) return cuda_fail(e, "stream");
+  double* out = nullptr;
+  unsigned long long* hist = nullptr;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const bool cnt = (flags & BP_FLAG_COUNT) != 0;
+  job->partials.assign((size_t)job->sb_count * BP_N_PAYOFFS * 2, 0.0);
+  job->hist.assign(66, 0ull);
+  do {
+    if ((e = cudaMallocAsync((void**)&out, sizeof(double) * job->partials.size(), st)) != cudaSuccess) {
+      cuda_fail(e, "alloc");
+      break;
+    }
+    if (cnt) {
+      if ((e = cudaMallocAsync((void**)&hist, sizeof(unsigned long long) * 66, st)) != cudaSuccess) {
+        cuda_fail(e, "alloc");
+        break;
+      }
+      cudaMemsetAsync(hist, 0, sizeof(unsigned long long) * 66, st);
+    }
+    cudaEventRecord(e0, st);
+    int rc = enqueue_superblocks(t, payoffs, flags, job->device, job->sb_first, job->sb_count, out, hist, st);
+    if (rc) {
+      setrc(rc);
+      break;
+    }
+    cudaEventRecord(e1, st);
+    cudaMemcpyAsync(job->partials.data(), out, sizeof(double) * job->partials.size(), cudaMemcpyDeviceToHost, st);
+    if (cnt) cudaMemcpyAsync(job->hist.data(), hist, sizeof(unsigned long long) * 66, cudaMemcpyDeviceToHost, st);
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) {
+      cuda_fail(e, "valuation");
+      break;
+    }
+    cudaEventElapsedTime(&job->ms, e0, e1);
+  } while (0);
+  if (out) cudaFreeAsync(out, st);
+  if (hist) cudaFreeAsync(hist, st);
+  cudaStreamSynchronize(st);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaStreamDestroy(st);
+}
+
+extern "C" int bp_exact(const bp_tree* tree, uint32_t payoffs, uint32_t flags, int n_dev, const int* devices,
+                        bp_exact_result* out) {
+  int rc = validate_tree(tree, 62);
+  if (rc) return rc;
+  if ((rc = kinds_ok(payoffs))) return rc;
+  if (!out) return fail(BP_E_INVALID_INPUT, "result pointer is NULL");
+  const int ndev_avail = bp_device_count();
+  if (ndev_avail < 1) return fail(BP_E_NO_DEVICE, "no CUDA device is visible");
+  std::vector<int> devs;
+  if (n_dev < 1 || !devices)
+    devs.push_back(0);
+  else
+    devs.assign(devices, devices + n_dev);
+  for (int d : devs)
+    if (d < 0 || d >= ndev_avail) return fail(BP_E_NO_DEVICE, "no CUDA device " + std::to_string(d));
+  const Layout lay = choose_layout(tree, payoffs, flags, nullptr);
+  const int G = std::min<int>((int)devs.size(), lay.n_sb);
+  std::vector<DeviceJob> jobs(G);
+  int first = 0;
+  for (int g = 0; g < G; ++g) {
+    const int cnt = lay.n_sb / G + (g < lay.n_sb % G ? 1 : 0);
+    jobs[g].device = devs[g];
+    jobs[g].sb_first = first;
+    jobs[g].sb_count = cnt;
+    first += cnt;
+  }
+  if (G == 1) {
+    run_device_job(tree, payoffs, flags, &jobs[0]);
+  } else {
+    std::vector<std::thread> th;
+    for (int g = 0; g < G; ++g) th.emplace_back(run_device_job, tree, payoffs, flags, &jobs[g]);
+    for (auto& x : th) x.join();
+  }
+  std::vector<double> all;
+  std::memset(out, 0, sizeof(*out));
+  float ms = 0.f;
+  for (auto& j : jobs) {
+    if (j.rc) return fail(j.rc, j.err);
+    all.insert(all.end(), j.partials.begin(), j.partials.end());
+    ms = std::max(ms, j.ms);
+    for (int i = 0; i < 64; ++i) out->hist[i] += j.hist[i];
+    out->leaves += j.hist[64];
+    out->code_sum += j.hist[65];
+  }
+  bp_combine_superblocks(all.data(), lay.n_sb, payoffs, out->value);
+  if (!(flags & BP_FLAG_COUNT)) out->leaves = 1ull << tree->n_steps;
+  out->kernel_ms = ms;
+  out->engine = lay.engine;
+  out->inner_bits = lay.L;
+  out->n_superblocks = lay.n_sb;
+  out->n_devices = G;
+  return BP_OK;
+}
+
+// ---------------------------------------------------------------------------
+extern "C" void bp_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+  philox4x32_10(ctr[0], ctr[1], ctr[2], ctr[3], key[0], key[1], out);
+}
+
+extern "C" int bp_fp64_peak(int device, double* dfma_per_s, double* sm_clock_mhz) {
+  if (device < 0 || device >= bp_device_count()) return fail(BP_E_NO_DEVICE, "no CUDA device " + std::to_string(device));
+  BP_CUDA(cudaSetDevice(device));
+  const int sms = device_sm_count(device);
+  const int grid = sms * 8;
+  double* buf = nullptr;
+  BP_CUDA(cudaMalloc((void**)&buf, sizeof(double) * grid * 256));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  BP_CUDA(launch_dfma_peak(buf, grid, 20, 0));
+  const int iters = 2000;
+  cudaEventRecord(e0, 0);
+  BP_CUDA(launch_dfma_peak(buf, grid, iters, 0));
+  cudaEventRecord(e1, 0);
+  BP_CUDA(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(buf);
+  const double ops = (double)grid * 256 * iters * 16 * 8;
+  if (dfma_per_s) *dfma_per_s = ops / (ms * 1e-3);
+  if (sm_clock_mhz) {
+    int khz = 0;
+    cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, device);
+    *sm_clock_mhz = khz / 1e3;
+  }
+  return BP_OK;
+}

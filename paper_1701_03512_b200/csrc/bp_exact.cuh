@@ -1,0 +1,92 @@
+// Exact 2^N path enumeration on B200 (sm_100a).
+//
+// Replaces the reference hot loop _rank_value (pkg/src/binpaths/exact.py:83-100),
+// which materialises a bool[CHUNK, N] bit matrix (paths.py:170-173), a row
+// product of per-step probabilities (exact.py:95) and a cumprod of the price
+// path (payoffs.py:103-104) for every path.
+//
+// Index decomposition (path code, step 1 = most significant bit, paths.py:1-12):
+//
+//   code = [ super-block | unit | lane | middle (m bits) | inner block (L bits) ]
+//           \____________ node index (D = N - L bits) ____________/
+//
+// * a warp owns a UNIT of 32 * 2^m consecutive nodes; lane i owns the 2^m
+//   nodes whose top D - m bits are (unit, i) -- its thread prefix;
+// * the thread walks its prefix once (S, running sum, max, min, up count),
+//   then visits its 2^m nodes with the middle tables (mid_*), then every
+//   leaf of each node in a fully unrolled block of 2^L leaves;
+// * every leaf is evaluated explicitly, but the affine structure of the
+//   payoffs turns the per-leaf work into ONE compare and ONE masked FMA:
+//     Asian:    sum_j S_j = Sig_node + S_node * c_s   (c_s = sum of the L
+//               relative prices of inner suffix s, a table)
+//     lookback: max_j S_j = max(Mx_node, S_node * mx_s)
+//   so "payoff > 0" is "c_s > theta_node" with theta = (N K - Sig)/S, and the
+//   leaf contributes S c_s + (Sig - N K).  Per up-count class c = |s| the
+//   block accumulates A_c = sum of c_s over in-the-money leaves and their
+//   count n_c; the node value is sum_c w[h + c] (S A_c + base n_c) with
+//   w[h] = e^{-qT} p^h (1-p)^{N-h} (exact.py:95,99 folded into one table).
+// * per-unit compensated partials -> fixed-order super-block reduce ->
+//   fixed-order combination of the (at most 8) super-blocks, so the result
+//   is bitwise independent of the number of GPUs that computed it.
+#pragma once
+#include <cstdint>
+#include "bp_common.cuh"
+
+namespace bp {
+
+// kind bit positions (include/binpaths_b200.h: bp_payoff)
+enum KindBit : int { kEC = 0, kEP = 1, kAP = 2, kFLP = 3, kAC = 4, kFL = 5 };
+constexpr int kNumKinds = 6;
+
+// table slot used by a kind in the fast engine; -1 = no per-leaf table
+BP_HD constexpr int kind_table(int k) {
+  return (k == kAC || k == kAP) ? 0 : (k == kFL) ? 1 : (k == kFLP) ? 2 : -1;
+}
+
+constexpr int kMidMax = 64;          // 2^m, m <= 6
+constexpr int kUnitTargetLog2 = 15;  // units >= 2^15 when the tree allows it
+constexpr int kMaxSB = 8;            // canonical super-blocks (top 3 bits)
+constexpr int kFastMinN = 16;        // smaller trees use the per-path walk
+constexpr unsigned kMaskHi = 0x01000000u;  // mask double 2^(16-1023)
+constexpr int kMaskExp = 1007;             // acc * 2^(1007 - a) = true sum
+
+struct ExactScalars {
+  double S0, K, NK, u, d, invN;
+  double sc_up[3];   // 2^a_t : table t scale (thresholds are scaled alike)
+  double sc_dn[3];   // 2^(1007 - a_t) : unscale of the masked sums
+  int N, L, D, m, Dp, n_mid;
+  int q;             // a unit is 2^q consecutive 32-lane prefix groups
+  int zero;          // opaque 0 (defeats constant hoisting in the leaf loop)
+  unsigned long long unit_first, unit_end;
+};
+
+template <int L>
+struct __align__(16) ExactArgs {
+  double tab[2][1 << L];  // scaled inner tables, two slots
+  double mid_c[kMidMax], mid_e[kMidMax], mid_mx[kMidMax], mid_mn[kMidMax];
+  int mid_h[kMidMax];
+  double w[kMaxN + 2];    // e^{-qT} p^h (1-p)^{N-h}, h = 0..N (zero padded)
+  double e_cls[L + 1];    // S_N / S_node for an inner suffix with c ups
+  double b_cls[L + 1];    // leaves per class, C(L, c)
+  ExactScalars s;
+};
+
+// Generic per-path walk (any per-step probabilities, any N, all kinds).
+struct GenericArgs {
+  double S0, K, u, d, disc, invN;
+  double p[kMaxN];        // per-step up probabilities
+  int N, g;               // 2^g codes per lane
+  unsigned kinds;
+  unsigned long long unit_first, unit_end;
+  unsigned long long n_codes;  // 2^N (saturating for N = 64 is not needed: N <= 62)
+};
+
+struct Layout {
+  int engine;   // 0 generic, 1 fast
+  int L, D, m, Dp, g, q;
+  unsigned long long units;
+  int n_sb;
+  unsigned long long units_per_sb;
+};
+
+}  // namespace bp

@@ -1,0 +1,54 @@
+// Internal launch interface between the kernel translation units and the
+// C ABI (bp_capi.cu).  Not part of the public header.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "bp_exact.cuh"
+
+namespace bp {
+
+bool fast_kind_mask_supported(unsigned km);
+cudaError_t launch_exact_fast(int L, unsigned km, const void* args, bool cnt, int grid, cudaStream_t st,
+                              double2* unit_out, unsigned long long* hist);
+int occupancy_exact_fast(int L, unsigned km, bool cnt);
+size_t exact_args_size(int L);
+
+cudaError_t launch_exact_generic(const GenericArgs& a, bool cnt, int grid, cudaStream_t st, double2* unit_out,
+                                 unsigned long long* hist);
+int occupancy_exact_generic(bool cnt);
+
+cudaError_t launch_sb_reduce(const double2* unit_out, unsigned long long units_per_sb, int sb_first, int sb_count,
+                             unsigned kinds, double scale_asian, double* out, cudaStream_t st);
+
+// Batched exact (one option per CTA group), see bp_batch_kernels.cu
+struct BatchOption {
+  double S0, K, u, d, p, disc;
+};
+cudaError_t launch_exact_batch(const BatchOption* opts_dev, int n_opts, int N, unsigned kind, double* values_dev,
+                               double2* scratch_dev, int ctas_per_option, cudaStream_t st);
+int batch_ctas_per_option(int N);
+
+// Monte Carlo, see bp_mc_kernels.cu
+struct McArgs {
+  double S0, K, u, d, invN;
+  uint32_t thr[kMaxN];   // Bernoulli thresholds floor(p_t 2^32) (saturated)
+  uint32_t always[2];    // bit t set: step t is always up (p_t == 1), 64 bits
+  int N, r;
+  unsigned kind;
+  uint32_t key0, key1;
+  uint32_t rep0;
+};
+cudaError_t launch_mc_strata(const McArgs& a, const unsigned long long* draws_dev,
+                             const unsigned long long* item_stratum_dev, const unsigned long long* item_first_dev,
+                             unsigned long long n_items, int n_reps, int n_strata, double* item_out_dev,
+                             double* theta_dev, double* sse_dev, const unsigned long long* stratum_item0_dev,
+                             cudaStream_t st);
+cudaError_t launch_mc_shared(const McArgs& a, unsigned long long R, const double* masses_dev, int n_reps,
+                             double* item_out_dev, unsigned long long n_items, unsigned long long items_per_rep,
+                             double* inner_mean_dev, double* inner_sse_dev, double* stratum_sum_dev,
+                             cudaStream_t st);
+
+cudaError_t launch_dfma_peak(double* out, int grid, int iters, cudaStream_t st);
+
+}  // namespace bp

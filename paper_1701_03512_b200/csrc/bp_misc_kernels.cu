@@ -1,0 +1,25 @@
+// K7: FP64-pipe peak microbenchmark (independent DFMA chains on every SM).
+// MEASURED_PEAKS.json carries no FP64 figure, so bench.py measures it live.
+#include "bp_kernels.h"
+
+namespace bp {
+
+__global__ void __launch_bounds__(256) k_dfma_peak(double* out, int iters, double a, double b) {
+  double x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6,
+         x7 = x0 + 7;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
+      x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+    }
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+}
+
+cudaError_t launch_dfma_peak(double* out, int grid, int iters, cudaStream_t st) {
+  k_dfma_peak<<<grid, 256, 0, st>>>(out, iters, 1.0000001, 1e-9);
+  return cudaGetLastError();
+}
+
+}  // namespace bp

@@ -1,0 +1,94 @@
+"""GPU parity of the exact engine against the CPU oracle and the reference goldens.
+
+Bar (BASELINE.json north_star): exact values within 1e-12 relative; leaf
+bookkeeping (paths per up count, total, code checksum) bit-exact.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1701_03512_b200 as bp
+from conftest import load_golden
+
+pytestmark = pytest.mark.gpu
+
+ALL = ["euro-call", "euro-put", "asian-put", "lookback-put", "asian-call", "float-lookback"]
+REL = 1e-12
+
+
+def _req(N, S0, K, q, T, u, d, probs, kind=bp.ASIAN_CALL, force=True):
+    params = bp.TreeParams(dt=T / N, u=u, d=d, beta=0.5 * (u + d), up_probs=np.broadcast_to(probs, (N,)))
+    inputs = bp.MarketInputs(S0=S0, K=K, q=q, sigma=0.2, T=T, N=N)
+    return bp.ValuationRequest(inputs=inputs, params=params, kind=kind, force_large=force)
+
+
+def _close(got, want, rel=REL, abs_=1e-13):
+    return abs(got - want) <= max(rel * abs(want), abs_)
+
+
+@pytest.mark.parametrize("generic", [False, True])
+def test_small_cases_all_kinds_vs_goldens(generic):
+    g = load_golden("exact_small.json")
+    for case in g["cases"] + g["medium"]:
+        N = case["N"]
+        probs = case.get("up_probs", [case.get("p")] * N)
+        req = _req(N, case["S0"], case["K"], case["q"], case["T"], case["u"], case["d"], np.array(probs))
+        res = bp.value_exact(req, kinds=[bp.resolve_kind(k) for k in ALL], generic=generic)
+        for k in ALL:
+            want = case["values"][k]
+            assert _close(res.values[k], want, rel=1e-11), (case["tag"], k, res.values[k], want)
+
+
+def test_config1_goldens_and_bookkeeping():
+    g = load_golden("exact_config1.json")
+    req = _req(20, 100.0, 100.0, 0.05, 1.0, g["u"], g["d"], g["p"])
+    res = bp.value_exact(req, kinds=[bp.ASIAN_CALL, bp.FLOATING_LOOKBACK, bp.PayoffKind.ASIAN_PUT,
+                                     bp.PayoffKind.FIXED_LOOKBACK_PUT], count=True)
+    assert res.engine == "affine-threshold"
+    assert _close(res.values["asian-call"], g["asian_call"])
+    assert _close(res.values["float-lookback"], g["float_lookback"])
+    assert _close(res.values["asian-put"], g["asian_put"])
+    assert _close(res.values["lookback-put"], g["fixed_lookback_put"])
+    assert [int(x) for x in res.hist] == [math.comb(20, h) for h in range(21)]
+    assert res.leaves == 1 << 20
+    assert res.code_sum == ((1 << 19) * ((1 << 20) - 1)) % (1 << 64)
+
+
+@pytest.mark.parametrize("N", [16, 17, 20, 23, 24])
+def test_fast_engine_matches_oracle(N):
+    rng = np.random.default_rng(N)
+    for _ in range(3):
+        S0 = float(rng.uniform(50, 150)); K = float(S0 * rng.uniform(0.8, 1.2))
+        r = float(rng.uniform(0.0, 0.08)); sigma = float(rng.uniform(0.1, 0.6)); T = float(rng.uniform(0.25, 3))
+        P = bp.classic_crr(N, sigma, r, T)
+        req = _req(N, S0, K, r, T, P.u, P.d, P.up_probs[0])
+        res = bp.value_exact(req, kinds=[bp.resolve_kind(k) for k in ALL], count=True)
+        want = oracle.exact(N, S0, K, P.u, P.d, P.up_probs[0], math.exp(-r * T), ALL, workers=16)
+        for k in ALL:
+            assert _close(res.values[k], want[k]), (N, k, res.values[k], want[k])
+        assert [int(x) for x in res.hist] == [math.comb(N, h) for h in range(N + 1)]
+
+
+def test_engines_agree_and_are_deterministic():
+    P = bp.classic_crr(22, 0.3, 0.03, 2.0)
+    req = _req(22, 100.0, 105.0, 0.03, 2.0, P.u, P.d, P.up_probs[0])
+    kinds = [bp.resolve_kind(k) for k in ALL]
+    a = bp.value_exact(req, kinds=kinds)
+    b = bp.value_exact(req, kinds=kinds)
+    c = bp.value_exact(req, kinds=kinds, generic=True)
+    for k in ALL:
+        assert a.values[k] == b.values[k]  # bitwise repeatable
+        assert _close(a.values[k], c.values[k]), (k, a.values[k], c.values[k])
+
+
+def test_drop_in_entry_points():
+    g = load_golden("exact_config1.json")
+    P = bp.classic_crr(20, 0.2, 0.05, 1.0)
+    inputs = bp.MarketInputs(S0=100.0, K=100.0, q=0.05, sigma=0.2, T=1.0, N=20)
+    for workers in (1, 2, 3, 8):
+        req = bp.ValuationRequest(inputs=inputs, params=P, kind=bp.ASIAN_CALL, workers=workers)
+        v = bp.value_exact_parallel(req)
+        assert v == bp.value_exact_serial(req)
+        assert _close(v, g["asian_call"])
