@@ -203,15 +203,15 @@ static int build_fast_args(const bp_tree* t, const Layout& lay, unsigned km, std
   double up[3] = {1, 1, 1}, dn[3] = {1, 1, 1};
   for (int i = 0; i < 3; ++i)
     if (!table_scale(*tabs[i], up[i], dn[i])) return fail(BP_E_INVALID_INPUT, "lattice outside the fast engine range");
-  // slot assignment: slot 0 = first table in use, slot 1 = second
-  int slot = 0;
-  const bool useT[3] = {(km & ((1u << kAC) | (1u << kAP))) != 0, (km & (1u << kFL)) != 0, (km & (1u << kFLP)) != 0};
-  for (int ti = 0; ti < 3; ++ti) {
-    if (!useT[ti]) continue;
-    if (slot > 1) return fail(BP_E_INVALID_INPUT, "more than two inner tables requested in one launch");
-    for (int s = 0; s < (1 << L); ++s) a.tab[slot][s] = (*tabs[ti])[s] * up[ti];
-    ++slot;
-  }
+  // tables in use: one -> tab[s]; two -> interleaved tab[2s + slot]
+  std::vector<int> use;
+  if (km & ((1u << kAC) | (1u << kAP))) use.push_back(0);
+  if (km & (1u << kFL)) use.push_back(1);
+  if (km & (1u << kFLP)) use.push_back(2);
+  if (use.size() > 2) return fail(BP_E_INVALID_INPUT, "more than two inner tables requested in one launch");
+  const int nt = (int)use.size();
+  for (int slot = 0; slot < nt; ++slot)
+    for (int s = 0; s < (1 << L); ++s) a.tab[nt == 1 ? s : 2 * s + slot] = (*tabs[use[slot]])[s] * up[use[slot]];
   // middle tables (chunk of m steps)
   const int m = lay.m;
   std::vector<double> mc, mmx, mmn, me;
@@ -282,6 +282,21 @@ static std::vector<unsigned> fast_groups(uint32_t payoffs) {
   return g;
 }
 
+// keep freed stream-ordered allocations in the device pool (scratch is
+// re-allocated every valuation; returning it to the OS costs milliseconds)
+static void keep_pool(int dev) {
+  static std::mutex mu;
+  static bool done[64] = {false};
+  std::lock_guard<std::mutex> g(mu);
+  if (dev < 0 || dev >= 64 || done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[dev] = true;
+}
+
 static int device_sm_count(int dev) {
   int n = 0;
   cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
@@ -302,6 +317,7 @@ static int enqueue_superblocks(const bp_tree* t, uint32_t payoffs, uint32_t flag
   const unsigned long long u0 = (unsigned long long)sb_first * lay.units_per_sb;
   const unsigned long long u1 = u0 + (unsigned long long)sb_count * lay.units_per_sb;
   const unsigned long long n_units = u1 - u0;
+  keep_pool(dev);
   double2* unit_out = nullptr;
   BP_CUDA(cudaMallocAsync((void**)&unit_out, sizeof(double2) * kNumKinds * n_units, st));
   // kernels index unit_out by absolute unit; shift the base pointer

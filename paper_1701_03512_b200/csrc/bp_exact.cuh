@@ -62,7 +62,9 @@ struct ExactScalars {
 
 template <int L>
 struct __align__(16) ExactArgs {
-  double tab[2][1 << L];  // scaled inner tables, two slots
+  // scaled inner tables: one table -> tab[s]; two tables -> interleaved
+  // (tab[2s] = first, tab[2s+1] = second) so one 16-byte load feeds a leaf
+  double tab[2 << L];
   double mid_c[kMidMax], mid_e[kMidMax], mid_mx[kMidMax], mid_mn[kMidMax];
   int mid_h[kMidMax];
   double w[kMaxN + 2];    // e^{-qT} p^h (1-p)^{N-h}, h = 0..N (zero padded)

@@ -24,8 +24,14 @@ k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_
                  kFLP_ = (KM >> kFLP) & 1, kEC_ = (KM >> kEC) & 1, kEP_ = (KM >> kEP) & 1;
   constexpr bool needMx = kFL_, needMn = kFLP_;
 
+  constexpr int NT_ = (int)(kAC_ || kAP_) + (int)kFL_ + (int)kFLP_;
   __shared__ double sw[kMaxN + 2 + NC];
   __shared__ unsigned long long shist[kMaxN + 2];
+  // two-table kernels read the interleaved tables from shared memory (one
+  // broadcast LDS.128 per leaf); one-table kernels read the constant bank
+  __shared__ __align__(16) double stab[NT_ == 2 ? (2 << L) : 2];
+  if (NT_ == 2)
+    for (int i = threadIdx.x; i < (2 << L); i += blockDim.x) stab[i] = a.tab[i];
   for (int i = threadIdx.x; i < kMaxN + 2 + NC; i += blockDim.x) sw[i] = (i < kMaxN + 2) ? a.w[i] : 0.0;
   if (CNT)
     for (int i = threadIdx.x; i < kMaxN + 2; i += blockDim.x) shist[i] = 0ull;
@@ -80,22 +86,21 @@ k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_
         cntC[c] = cntP[c] = cntX[c] = cntN[c] = 0u;
       }
       const int off = j & sc.zero;  // 0, opaque to the compiler
-      const double2* t0 = reinterpret_cast<const double2*>(a.tab[0]) + off;
-      const double2* t1 = reinterpret_cast<const double2*>(a.tab[1]) + off;
+      constexpr int NT = (int)(kAC_ || kAP_) + (int)kFL_ + (int)kFLP_;  // tables in use (<= 2)
+      const double2* tb = reinterpret_cast<const double2*>(NT == 2 ? stab : a.tab) + off;
 #pragma unroll
       for (int s2 = 0; s2 < NL / 2; ++s2) {
-        double2 v0 = make_double2(0.0, 0.0), v1 = make_double2(0.0, 0.0);
-        // slot 0 always holds the first table in use, slot 1 the second
-        constexpr bool use0 = kAC_ || kAP_ || kFL_ || kFLP_;
-        constexpr bool use1 = (kAC_ || kAP_) ? (kFL_ || kFLP_) : (kFL_ && kFLP_);
-        if (use0) v0 = t0[s2];
-        if (use1) v1 = t1[s2];
+        // NT == 1: one double2 = leaves (2 s2, 2 s2 + 1) of the single table
+        // NT == 2: two double2 = (first, second) table values of the two leaves
+        double2 va = make_double2(0.0, 0.0), vb = make_double2(0.0, 0.0);
+        if (NT == 1) va = tb[s2];
+        if (NT == 2) { va = tb[2 * s2]; vb = tb[2 * s2 + 1]; }
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
           const int s = 2 * s2 + hh;
           const int cls = __popc(s);
-          const double x0 = hh ? v0.y : v0.x;
-          const double x1 = hh ? v1.y : v1.x;
+          const double x0 = (NT == 1) ? (hh ? va.y : va.x) : (hh ? vb.x : va.x);
+          const double x1 = (NT == 1) ? 0.0 : (hh ? vb.y : va.y);
           if (kAC_ || kAP_) {
             const double c = x0;
             if (kAC_) {
