@@ -16,6 +16,9 @@ from .paths import (BernoulliPath, PathPartition, block_code_ranges, block_proba
                     make_partition, path_probability)
 from .payoffs import (ASIAN_CALL, FLOATING_LOOKBACK, GpuPayoff, PayoffKind, kind_bit, parse_payoff, payoff,
                       payoff_batch, resolve_kind)
+from .mc import (Estimate, McConfig, PhiloxStream, RepetitionSummary, allocate_strata, estimate_basic,
+                 estimate_partitioned, estimate_partitioned_equal, estimate_shared, mc_stream, run_repetitions,
+                 sample_path)
 from .exact import (LARGE_DEPTH, ExactResult, ValuationRequest, value_exact, value_exact_parallel,
                     value_exact_serial, value_leaf_formula)
 

@@ -555,3 +555,198 @@ extern "C" int bp_fp64_peak(int device, double* dfma_per_s, double* sm_clock_mhz
   }
   return BP_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Monte Carlo (mc.py:92-100,135-159,197-213,287-331)
+static int single_kind(uint32_t payoff, unsigned* bit) {
+  if (payoff == 0 || (payoff & (payoff - 1)) || (payoff >> BP_N_PAYOFFS))
+    return fail(BP_E_INVALID_INPUT, "Monte Carlo takes exactly one payoff bit");
+  *bit = (unsigned)__builtin_ctz(payoff);
+  return BP_OK;
+}
+
+static void fill_mc_args(const bp_tree* t, unsigned kind, int r, uint64_t seed, uint32_t rep0, McArgs& a) {
+  std::memset(&a, 0, sizeof(a));
+  a.S0 = t->S0;
+  a.K = t->K;
+  a.u = t->u;
+  a.d = t->d;
+  a.invN = 1.0 / t->n_steps;
+  a.N = t->n_steps;
+  a.r = r;
+  a.kind = kind;
+  a.key0 = (uint32_t)(seed & 0xffffffffull);
+  a.key1 = (uint32_t)(seed >> 32);
+  a.rep0 = rep0;
+  for (int i = 0; i < t->n_steps; ++i) {
+    const double p = t->up_probs[i];
+    uint32_t thr = 0;
+    if (p >= 1.0) {
+      thr = 0xffffffffu;
+      a.always[i / 32] |= 1u << (i % 32);
+    } else if (p > 0.0) {
+      thr = (uint32_t)std::floor(p * 4294967296.0);
+    }
+    a.thr[i] = thr;
+  }
+}
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  cudaStream_t st = 0;
+  ~DevBuf() {
+    if (p) cudaFreeAsync(p, st);
+  }
+};
+
+extern "C" int bp_mc_strata(const bp_tree* tree, uint32_t payoff, int r, const uint64_t* draws, uint64_t seed,
+                            uint32_t rep0, uint32_t n_reps, int device, double* theta, double* sse,
+                            double* kernel_ms) {
+  int rc = validate_tree(tree, 64);
+  if (rc) return rc;
+  unsigned kind;
+  if ((rc = single_kind(payoff, &kind))) return rc;
+  if (r < 0 || r > tree->n_steps || r > 24) return fail(BP_E_INVALID_INPUT, "prefix bits r out of range");
+  if (!draws || !theta || !sse || n_reps < 1) return fail(BP_E_INVALID_INPUT, "bad Monte Carlo buffers");
+  if (device < 0 || device >= bp_device_count()) return fail(BP_E_NO_DEVICE, "no CUDA device " + std::to_string(device));
+  const int M = 1 << r;
+  for (int m = 0; m < M; ++m)
+    if (draws[m] >= (1ull << 32)) return fail(BP_E_INVALID_INPUT, "at most 2^32 - 1 draws per stratum");
+  // work items of one repetition, stratum-ascending
+  const unsigned long long CH = mc_chunk();
+  std::vector<unsigned long long> item_stratum, item_first, stratum_item0(M + 1, 0);
+  for (int m = 0; m < M; ++m) {
+    stratum_item0[m] = item_stratum.size();
+    for (unsigned long long f = 0; f < draws[m]; f += CH) {
+      item_stratum.push_back(m);
+      item_first.push_back(f);
+    }
+  }
+  stratum_item0[M] = item_stratum.size();
+  const unsigned long long items_per_rep = item_stratum.size();
+  BP_CUDA(cudaSetDevice(device));
+  keep_pool(device);
+  cudaStream_t st;
+  BP_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  struct StreamGuard {
+    cudaStream_t s;
+    ~StreamGuard() {
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    }
+  } sg{st};
+  McArgs a;
+  fill_mc_args(tree, kind, r, seed, rep0, a);
+  DevBuf<unsigned long long> d_draws, d_is, d_if, d_i0;
+  DevBuf<double> d_items, d_theta, d_sse;
+  d_draws.st = d_is.st = d_if.st = d_i0.st = d_items.st = d_theta.st = d_sse.st = st;
+  const size_t ni = std::max<size_t>(1, items_per_rep);
+  BP_CUDA(cudaMallocAsync((void**)&d_draws.p, sizeof(unsigned long long) * M, st));
+  BP_CUDA(cudaMallocAsync((void**)&d_is.p, sizeof(unsigned long long) * ni, st));
+  BP_CUDA(cudaMallocAsync((void**)&d_if.p, sizeof(unsigned long long) * ni, st));
+  BP_CUDA(cudaMallocAsync((void**)&d_i0.p, sizeof(unsigned long long) * (M + 1), st));
+  BP_CUDA(cudaMallocAsync((void**)&d_items.p, sizeof(double) * 3 * ni * n_reps, st));
+  BP_CUDA(cudaMallocAsync((void**)&d_theta.p, sizeof(double) * (size_t)M * n_reps, st));
+  BP_CUDA(cudaMallocAsync((void**)&d_sse.p, sizeof(double) * (size_t)M * n_reps, st));
+  BP_CUDA(cudaMemcpyAsync(d_draws.p, draws, sizeof(unsigned long long) * M, cudaMemcpyHostToDevice, st));
+  if (items_per_rep) {
+    BP_CUDA(cudaMemcpyAsync(d_is.p, item_stratum.data(), sizeof(unsigned long long) * items_per_rep,
+                            cudaMemcpyHostToDevice, st));
+    BP_CUDA(cudaMemcpyAsync(d_if.p, item_first.data(), sizeof(unsigned long long) * items_per_rep,
+                            cudaMemcpyHostToDevice, st));
+  }
+  BP_CUDA(cudaMemcpyAsync(d_i0.p, stratum_item0.data(), sizeof(unsigned long long) * (M + 1),
+                          cudaMemcpyHostToDevice, st));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, st);
+  BP_CUDA(launch_mc_strata(a, d_draws.p, d_is.p, d_if.p, items_per_rep, (int)n_reps, M, d_items.p, d_theta.p,
+                           d_sse.p, d_i0.p, st));
+  cudaEventRecord(e1, st);
+  BP_CUDA(cudaMemcpyAsync(theta, d_theta.p, sizeof(double) * (size_t)M * n_reps, cudaMemcpyDeviceToHost, st));
+  BP_CUDA(cudaMemcpyAsync(sse, d_sse.p, sizeof(double) * (size_t)M * n_reps, cudaMemcpyDeviceToHost, st));
+  BP_CUDA(cudaStreamSynchronize(st));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (kernel_ms) *kernel_ms = ms;
+  return BP_OK;
+}
+
+extern "C" int bp_mc_shared(const bp_tree* tree, uint32_t payoff, int r, uint64_t R, const double* masses,
+                            uint64_t seed, uint32_t rep0, uint32_t n_reps, int device, double* inner_mean,
+                            double* inner_sse, double* stratum_means, double* kernel_ms) {
+  int rc = validate_tree(tree, 64);
+  if (rc) return rc;
+  unsigned kind;
+  if ((rc = single_kind(payoff, &kind))) return rc;
+  if (r < 0 || r > tree->n_steps || r > 16) return fail(BP_E_INVALID_INPUT, "prefix bits r out of range");
+  if (R < 1 || R >= (1ull << 32)) return fail(BP_E_INVALID_INPUT, "R must be in [1, 2^32)");
+  if (!masses || !inner_mean || !inner_sse || !stratum_means || n_reps < 1)
+    return fail(BP_E_INVALID_INPUT, "bad Monte Carlo buffers");
+  if (device < 0 || device >= bp_device_count()) return fail(BP_E_NO_DEVICE, "no CUDA device " + std::to_string(device));
+  const int M = 1 << r;
+  // prefix states (S, sum, max, min) after the r prefix steps of every stratum
+  std::vector<double> pre(4 * (size_t)M);
+  for (int m = 0; m < M; ++m) {
+    double S = tree->S0, sum = 0.0, mx = -INFINITY, mn = INFINITY;
+    for (int t = 0; t < r; ++t) {
+      const int b = (m >> (r - 1 - t)) & 1;
+      S *= b ? tree->u : tree->d;
+      sum += S;
+      mx = std::max(mx, S);
+      mn = std::min(mn, S);
+    }
+    pre[4 * m] = S;
+    pre[4 * m + 1] = sum;
+    pre[4 * m + 2] = mx;
+    pre[4 * m + 3] = mn;
+  }
+  const unsigned long long CH = mc_chunk();
+  const unsigned long long items_per_rep = (R + CH - 1) / CH;
+  BP_CUDA(cudaSetDevice(device));
+  keep_pool(device);
+  cudaStream_t st;
+  BP_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  struct StreamGuard {
+    cudaStream_t s;
+    ~StreamGuard() {
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    }
+  } sg{st};
+  McArgs a;
+  fill_mc_args(tree, kind, r, seed, rep0, a);
+  DevBuf<double> d_m, d_pre, d_items, d_ws, d_im, d_is, d_sm;
+  d_m.st = d_pre.st = d_items.st = d_ws.st = d_im.st = d_is.st = d_sm.st = st;
+  const size_t nit = (size_t)items_per_rep * n_reps;
+  BP_CUDA(cudaMallocAsync((void**)&d_m.p, sizeof(double) * M, st));
+  BP_CUDA(cudaMallocAsync((void**)&d_pre.p, sizeof(double) * 4 * M, st));
+  BP_CUDA(cudaMallocAsync((void**)&d_items.p, sizeof(double) * 3 * nit, st));
+  BP_CUDA(cudaMallocAsync((void**)&d_ws.p, sizeof(double) * 8 * nit * M, st));
+  BP_CUDA(cudaMallocAsync((void**)&d_im.p, sizeof(double) * n_reps, st));
+  BP_CUDA(cudaMallocAsync((void**)&d_is.p, sizeof(double) * n_reps, st));
+  BP_CUDA(cudaMallocAsync((void**)&d_sm.p, sizeof(double) * (size_t)M * n_reps, st));
+  BP_CUDA(cudaMemcpyAsync(d_m.p, masses, sizeof(double) * M, cudaMemcpyHostToDevice, st));
+  BP_CUDA(cudaMemcpyAsync(d_pre.p, pre.data(), sizeof(double) * 4 * M, cudaMemcpyHostToDevice, st));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, st);
+  BP_CUDA(launch_mc_shared(a, R, d_m.p, d_pre.p, M, (int)n_reps, d_items.p, d_ws.p, items_per_rep, d_im.p, d_is.p,
+                           d_sm.p, st));
+  cudaEventRecord(e1, st);
+  BP_CUDA(cudaMemcpyAsync(inner_mean, d_im.p, sizeof(double) * n_reps, cudaMemcpyDeviceToHost, st));
+  BP_CUDA(cudaMemcpyAsync(inner_sse, d_is.p, sizeof(double) * n_reps, cudaMemcpyDeviceToHost, st));
+  BP_CUDA(cudaMemcpyAsync(stratum_means, d_sm.p, sizeof(double) * (size_t)M * n_reps, cudaMemcpyDeviceToHost, st));
+  BP_CUDA(cudaStreamSynchronize(st));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (kernel_ms) *kernel_ms = ms;
+  return BP_OK;
+}

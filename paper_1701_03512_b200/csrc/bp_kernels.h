@@ -33,7 +33,7 @@ int batch_ctas_per_option(int N);
 struct McArgs {
   double S0, K, u, d, invN;
   uint32_t thr[kMaxN];   // Bernoulli thresholds floor(p_t 2^32) (saturated)
-  uint32_t always[2];    // bit t set: step t is always up (p_t == 1), 64 bits
+  uint32_t always[2];    // bit t set: step t is always up (p_t >= 1)
   int N, r;
   unsigned kind;
   uint32_t key0, key1;
@@ -41,13 +41,14 @@ struct McArgs {
 };
 cudaError_t launch_mc_strata(const McArgs& a, const unsigned long long* draws_dev,
                              const unsigned long long* item_stratum_dev, const unsigned long long* item_first_dev,
-                             unsigned long long n_items, int n_reps, int n_strata, double* item_out_dev,
+                             unsigned long long items_per_rep, int n_reps, int n_strata, double* item_out_dev,
                              double* theta_dev, double* sse_dev, const unsigned long long* stratum_item0_dev,
                              cudaStream_t st);
-cudaError_t launch_mc_shared(const McArgs& a, unsigned long long R, const double* masses_dev, int n_reps,
-                             double* item_out_dev, unsigned long long n_items, unsigned long long items_per_rep,
-                             double* inner_mean_dev, double* inner_sse_dev, double* stratum_sum_dev,
-                             cudaStream_t st);
+cudaError_t launch_mc_shared(const McArgs& a, unsigned long long R, const double* masses_dev, const double* pre_tab_dev,
+                             int M, int n_reps, double* item_out_dev, double* warp_sums_dev,
+                             unsigned long long items_per_rep, double* inner_mean_dev, double* inner_sse_dev,
+                             double* stratum_means_dev, cudaStream_t st);
+unsigned long long mc_chunk();
 
 cudaError_t launch_dfma_peak(double* out, int grid, int iters, cudaStream_t st);
 

@@ -1,0 +1,307 @@
+// Monte Carlo kernels: stratified ("partitioned") MC and its k = 0 special
+// case (basic MC), and the shared-sample estimator.
+//
+// Reference: pkg/src/binpaths/mc.py -- _stratum_stats (:197-213), sampler
+// sample_bits (:98-100) keyed by mc_stream(seed, stratum, rep) (:92-95),
+// estimate_shared's draw loop (:287-331).
+//
+// Stream layout (replaces numpy Philox(SeedSequence(seed, spawn_key=(m, rep)))):
+//   key     = (seed mod 2^32, seed >> 32)
+//   counter = (word block j, draw index i, stream id m, repetition)
+//   suffix step w (0-based after the r prefix steps) uses 32-bit word w % 4
+//   of block j = w / 4; up iff word < floor(p_t 2^32) (p_t == 1: always).
+// Streams are disjoint by construction and independent of the thread
+// mapping, so results do not depend on the grid, the GPU count or timing.
+//
+// Work items: (rep, stratum, chunk of kChunk draws).  A CTA evaluates one
+// item: thread t takes draws chunk_base + t + 256 k, keeps a Welford
+// (n, mean, M2), the CTA merges them with Chan's formula in a fixed tree,
+// and a second kernel merges the items of a stratum in ascending order.
+#include "bp_kernels.h"
+
+namespace bp {
+
+constexpr int kMcThreads = 256;
+constexpr unsigned long long kChunk = 4096;  // draws per work item
+
+struct Welford {
+  double n, mean, m2;
+};
+
+__device__ __forceinline__ Welford chan(const Welford& a, const Welford& b) {
+  if (b.n == 0.0) return a;
+  if (a.n == 0.0) return b;
+  const double n = a.n + b.n;
+  const double delta = b.mean - a.mean;
+  const double f = b.n / n;
+  Welford r;
+  r.n = n;
+  r.mean = fma(delta, f, a.mean);
+  r.m2 = a.m2 + b.m2 + delta * delta * a.n * f;
+  return r;
+}
+
+// fixed-order CTA merge of per-thread Welford states; thread 0 gets the total
+__device__ Welford cta_merge(Welford w) {
+  __shared__ double sn[kMcThreads], smean[kMcThreads], sm2[kMcThreads];
+  sn[threadIdx.x] = w.n;
+  smean[threadIdx.x] = w.mean;
+  sm2[threadIdx.x] = w.m2;
+  __syncthreads();
+  for (int stride = kMcThreads / 2; stride > 0; stride >>= 1) {
+    if (threadIdx.x < stride) {
+      Welford a{sn[threadIdx.x], smean[threadIdx.x], sm2[threadIdx.x]};
+      Welford b{sn[threadIdx.x + stride], smean[threadIdx.x + stride], sm2[threadIdx.x + stride]};
+      Welford c = chan(a, b);
+      sn[threadIdx.x] = c.n;
+      smean[threadIdx.x] = c.mean;
+      sm2[threadIdx.x] = c.m2;
+    }
+    __syncthreads();
+  }
+  Welford r{sn[0], smean[0], sm2[0]};
+  __syncthreads();
+  return r;
+}
+
+// Path state after the r prefix steps of stratum m (the prefix is fixed).
+struct PathState {
+  double S, sum, mx, mn;
+};
+
+__device__ __forceinline__ PathState prefix_state(const McArgs& a, unsigned long long m) {
+  PathState st{a.S0, 0.0, -INFINITY, INFINITY};
+  for (int t = 0; t < a.r; ++t) {
+    const int b = (int)((m >> (a.r - 1 - t)) & 1ull);
+    st.S *= b ? a.u : a.d;
+    st.sum += st.S;
+    st.mx = fmax(st.mx, st.S);
+    st.mn = fmin(st.mn, st.S);
+  }
+  return st;
+}
+
+__device__ __forceinline__ double payoff_of(unsigned kind, const PathState& st, double K, int N) {
+  const double mean = st.sum / (double)N;
+  switch (kind) {
+    case kEC: return fmax(st.S - K, 0.0);
+    case kEP: return fmax(K - st.S, 0.0);
+    case kAP: return fmax(K - mean, 0.0);
+    case kFLP: return fmax(K - st.mn, 0.0);
+    case kAC: return fmax(mean - K, 0.0);
+    default: return st.mx - st.S;
+  }
+}
+
+// Walk the N - r suffix steps of draw i on stream (m, rep) from state st.
+template <unsigned KIND>
+__device__ __forceinline__ PathState walk_suffix(const McArgs& a, PathState st, uint32_t i, uint32_t stream,
+                                                 uint32_t rep) {
+  constexpr bool need_max = KIND == kFL;
+  constexpr bool need_min = KIND == kFLP;
+  constexpr bool need_sum = KIND == kAC || KIND == kAP;
+  const int nsuf = a.N - a.r;
+  uint32_t blk[4];
+  for (int j = 0; 4 * j < nsuf; ++j) {
+    philox4x32_10((uint32_t)j, i, stream, rep, a.key0, a.key1, blk);
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      const int w = 4 * j + l;
+      if (w < nsuf) {
+        const int t = a.r + w;
+        const bool up = (blk[l] < a.thr[t]) || ((t < 32 ? (a.always[0] >> t) : (a.always[1] >> (t - 32))) & 1u);
+        st.S *= up ? a.u : a.d;
+        if (need_sum) st.sum += st.S;
+        if (need_max) st.mx = fmax(st.mx, st.S);
+        if (need_min) st.mn = fmin(st.mn, st.S);
+      }
+    }
+  }
+  return st;
+}
+
+// ---------------------------------------------------------------------------
+// K4/K5: one CTA per work item (grid-stride).  item -> (rep k, stratum m, first draw)
+template <unsigned KIND>
+__global__ void __launch_bounds__(kMcThreads)
+k_mc_strata(const __grid_constant__ McArgs a, const unsigned long long* __restrict__ draws,
+            const unsigned long long* __restrict__ item_stratum, const unsigned long long* __restrict__ item_first,
+            unsigned long long items_per_rep, int n_reps, double* __restrict__ item_out) {
+  const unsigned long long n_items = items_per_rep * (unsigned long long)n_reps;
+  for (unsigned long long it = blockIdx.x; it < n_items; it += gridDim.x) {
+    const unsigned long long k = it / items_per_rep, li = it % items_per_rep;
+    const unsigned long long m = item_stratum[li];
+    const unsigned long long first = item_first[li];
+    const unsigned long long R = draws[m];
+    const unsigned long long last = first + kChunk < R ? first + kChunk : R;
+    const PathState pre = prefix_state(a, m);
+    Welford w{0.0, 0.0, 0.0};
+    for (unsigned long long i = first + threadIdx.x; i < last; i += kMcThreads) {
+      const PathState st = walk_suffix<KIND>(a, pre, (uint32_t)i, (uint32_t)m, a.rep0 + (uint32_t)k);
+      const double v = payoff_of(KIND, st, a.K, a.N);
+      w.n += 1.0;
+      const double delta = v - w.mean;
+      w.mean += delta / w.n;
+      w.m2 = fma(delta, v - w.mean, w.m2);
+    }
+    const Welford t = cta_merge(w);
+    if (threadIdx.x == 0) {
+      item_out[it * 3 + 0] = t.n;
+      item_out[it * 3 + 1] = t.mean;
+      item_out[it * 3 + 2] = t.m2;
+    }
+  }
+}
+
+// ascending-order merge of a stratum's items -> theta, sse
+__global__ void k_mc_strata_merge(const double* __restrict__ item_out, const unsigned long long* __restrict__ stratum_item0,
+                                  unsigned long long items_per_rep, int n_strata, int n_reps,
+                                  double* __restrict__ theta, double* __restrict__ sse) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= (long long)n_strata * n_reps) return;
+  const long long k = idx / n_strata, m = idx % n_strata;
+  const unsigned long long i0 = stratum_item0[m], i1 = stratum_item0[m + 1];
+  Welford acc{0.0, 0.0, 0.0};
+  for (unsigned long long i = i0; i < i1; ++i) {
+    const unsigned long long it = (unsigned long long)k * items_per_rep + i;
+    Welford b{item_out[it * 3], item_out[it * 3 + 1], item_out[it * 3 + 2]};
+    acc = chan(acc, b);
+  }
+  theta[idx] = acc.n > 0.0 ? acc.mean : 0.0;
+  sse[idx] = acc.n > 0.0 ? acc.m2 : 0.0;
+}
+
+cudaError_t launch_mc_strata(const McArgs& a, const unsigned long long* draws_dev,
+                             const unsigned long long* item_stratum_dev, const unsigned long long* item_first_dev,
+                             unsigned long long items_per_rep, int n_reps, int n_strata, double* item_out_dev,
+                             double* theta_dev, double* sse_dev, const unsigned long long* stratum_item0_dev,
+                             cudaStream_t st) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned long long n_items = items_per_rep * (unsigned long long)n_reps;
+  if (n_items) {
+    const int grid = (int)(n_items < (unsigned long long)sms * 16 ? n_items : (unsigned long long)sms * 16);
+#define BP_MC_CASE(K) \
+  case K: k_mc_strata<K><<<grid, kMcThreads, 0, st>>>(a, draws_dev, item_stratum_dev, item_first_dev, items_per_rep, n_reps, item_out_dev); break;
+    switch (a.kind) {
+      BP_MC_CASE(kEC) BP_MC_CASE(kEP) BP_MC_CASE(kAP) BP_MC_CASE(kFLP) BP_MC_CASE(kAC) BP_MC_CASE(kFL)
+      default: return cudaErrorInvalidValue;
+    }
+#undef BP_MC_CASE
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  const long long total = (long long)n_strata * n_reps;
+  k_mc_strata_merge<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(item_out_dev, stratum_item0_dev, items_per_rep,
+                                                                      n_strata, n_reps, theta_dev, sse_dev);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Shared-sample MC: draw i's suffix is drawn once (stream 0) and evaluated
+// under all M prefixes.  Per item: Welford of the inner sums + per-warp,
+// per-stratum payoff sums (fixed order, no atomics).
+template <unsigned KIND>
+__global__ void __launch_bounds__(kMcThreads)
+k_mc_shared(const __grid_constant__ McArgs a, unsigned long long R, const double* __restrict__ masses,
+            const double* __restrict__ pre_tab /* [M][4] S, sum, mx, mn after r steps */, int M,
+            unsigned long long items_per_rep, int n_reps, double* __restrict__ item_out,
+            double* __restrict__ warp_sums /* [item][8][M] */) {
+  const unsigned long long n_items = items_per_rep * (unsigned long long)n_reps;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (unsigned long long it = blockIdx.x; it < n_items; it += gridDim.x) {
+    const unsigned long long k = it / items_per_rep, li = it % items_per_rep;
+    const unsigned long long first = li * kChunk;
+    const unsigned long long last = first + kChunk < R ? first + kChunk : R;
+    double* ws = warp_sums + (it * 8 + warp) * (unsigned long long)M;
+    for (int m = lane; m < M; m += 32) ws[m] = 0.0;
+    __syncwarp();
+    Welford w{0.0, 0.0, 0.0};
+    // iterate in warp-synchronous rounds so the per-stratum warp reduce is uniform
+    for (unsigned long long base = first + warp * 32; base < last; base += kMcThreads) {
+      const unsigned long long i = base + lane;
+      const bool live = i < last;
+      // suffix relative to a unit start price
+      PathState rel{1.0, 0.0, -INFINITY, INFINITY};
+      if (live) rel = walk_suffix<KIND>(a, rel, (uint32_t)i, 0u, a.rep0 + (uint32_t)k);
+      double inner = 0.0;
+      for (int m = 0; m < M; ++m) {
+        const double S = pre_tab[4 * m], sum = pre_tab[4 * m + 1], mx = pre_tab[4 * m + 2], mn = pre_tab[4 * m + 3];
+        PathState st{S * rel.S, fma(S, rel.sum, sum), fmax(mx, S * rel.mx), fmin(mn, S * rel.mn)};
+        const double v = live ? payoff_of(KIND, st, a.K, a.N) : 0.0;
+        inner = fma(masses[m], v, inner);
+        double s = v;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (lane == 0) ws[m] += s;
+      }
+      if (live) {
+        w.n += 1.0;
+        const double delta = inner - w.mean;
+        w.mean += delta / w.n;
+        w.m2 = fma(delta, inner - w.mean, w.m2);
+      }
+    }
+    const Welford t = cta_merge(w);
+    if (threadIdx.x == 0) {
+      item_out[it * 3 + 0] = t.n;
+      item_out[it * 3 + 1] = t.mean;
+      item_out[it * 3 + 2] = t.m2;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void k_mc_shared_merge(const double* __restrict__ item_out, const double* __restrict__ warp_sums,
+                                  unsigned long long items_per_rep, int M, int n_reps, double Rd,
+                                  double* __restrict__ inner_mean, double* __restrict__ inner_sse,
+                                  double* __restrict__ stratum_means) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx < n_reps) {
+    Welford acc{0.0, 0.0, 0.0};
+    for (unsigned long long i = 0; i < items_per_rep; ++i) {
+      const unsigned long long it = (unsigned long long)idx * items_per_rep + i;
+      acc = chan(acc, Welford{item_out[it * 3], item_out[it * 3 + 1], item_out[it * 3 + 2]});
+    }
+    inner_mean[idx] = acc.mean;
+    inner_sse[idx] = acc.m2;
+  }
+  if (idx < (long long)M * n_reps) {
+    const long long k = idx / M, m = idx % M;
+    double s = 0.0, c = 0.0;
+    for (unsigned long long i = 0; i < items_per_rep; ++i)
+      for (int wp = 0; wp < 8; ++wp)
+        comp_add(s, c, warp_sums[(((unsigned long long)k * items_per_rep + i) * 8 + wp) * (unsigned long long)M + m]);
+    stratum_means[idx] = (s + c) / Rd;
+  }
+}
+
+cudaError_t launch_mc_shared(const McArgs& a, unsigned long long R, const double* masses_dev, const double* pre_tab_dev,
+                             int M, int n_reps, double* item_out_dev, double* warp_sums_dev,
+                             unsigned long long items_per_rep, double* inner_mean_dev, double* inner_sse_dev,
+                             double* stratum_means_dev, cudaStream_t st) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned long long n_items = items_per_rep * (unsigned long long)n_reps;
+  const int grid = (int)(n_items < (unsigned long long)sms * 16 ? n_items : (unsigned long long)sms * 16);
+#define BP_SH_CASE(K) \
+  case K: k_mc_shared<K><<<grid, kMcThreads, 0, st>>>(a, R, masses_dev, pre_tab_dev, M, items_per_rep, n_reps, item_out_dev, warp_sums_dev); break;
+  switch (a.kind) {
+    BP_SH_CASE(kEC) BP_SH_CASE(kEP) BP_SH_CASE(kAP) BP_SH_CASE(kFLP) BP_SH_CASE(kAC) BP_SH_CASE(kFL)
+    default: return cudaErrorInvalidValue;
+  }
+#undef BP_SH_CASE
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const long long total = (long long)M * n_reps > n_reps ? (long long)M * n_reps : n_reps;
+  k_mc_shared_merge<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(item_out_dev, warp_sums_dev, items_per_rep, M,
+                                                                      n_reps, (double)R, inner_mean_dev, inner_sse_dev,
+                                                                      stratum_means_dev);
+  return cudaGetLastError();
+}
+
+unsigned long long mc_chunk() { return kChunk; }
+
+}  // namespace bp

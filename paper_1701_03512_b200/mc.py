@@ -1,0 +1,321 @@
+"""Monte Carlo estimators -- drop-in for pkg/src/binpaths/mc.py.
+
+Same names, signatures, return types and exceptions as the reference's
+``estimate_basic`` (:135-159), ``estimate_partitioned`` (:234-257),
+``estimate_partitioned_equal`` (:260-284), ``estimate_shared`` (:287-331),
+``allocate_strata`` (:162-194) and ``run_repetitions`` (:334-353).
+
+The draws and the per-stratum statistics (theta_m, SSE_m) run in the CUDA
+engine (bp_mc_strata / bp_mc_shared).  The random stream is Philox4x32-10
+keyed by (seed, stratum, rep) in its counter (include/binpaths_b200.h), the
+GPU counterpart of the reference's mc_stream(seed, stratum, rep) keying:
+reproducible, independent of thread / GPU mapping, M = 1 bit-identical to
+basic MC.  Individual draws differ from numpy's Philox4x64 stream, so parity
+with the reference is statistical (tests/test_mc_parity.py), while parity
+with the CPU oracle, which draws the same bits, is to rounding.
+
+Host-side arithmetic here is O(M): allocation, stratum masses and the
+final combination, kept in the reference's order so per-stratum identities
+(e.g. value == disc * sum(theta * mass)) hold bit for bit.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+from typing import Callable, Optional
+
+import numpy as np
+
+from . import _native
+from .errors import InfeasibleAllocation, InvalidInput, InvalidWorkerCount
+from .paths import BernoulliPath, PathPartition, block_probability, make_partition
+from .payoffs import kind_bit
+
+
+def _pos_int(x) -> bool:
+    return isinstance(x, int) and not isinstance(x, bool)
+
+
+@dataclass(frozen=True)
+class McConfig:
+    """Sampling plan: total draws R, stratum count M, seed, repetitions."""
+
+    R: int
+    M: int = 1
+    seed: int = 0
+    reps: int = 1
+
+    def __post_init__(self):
+        for name, lo in (("R", 1), ("M", 1), ("seed", 0), ("reps", 1)):
+            v = getattr(self, name)
+            if not _pos_int(v) or v < lo:
+                want = "a nonnegative integer" if lo == 0 else "a positive integer"
+                raise InvalidInput(f"{name} must be {want}, got {v!r}")
+
+
+@dataclass(frozen=True)
+class Estimate:
+    value: float
+    variance: float
+    std_error: float
+    R_used: int
+    method: str
+    seed: int
+    per_stratum: Optional[tuple] = None
+
+
+@dataclass(frozen=True)
+class RepetitionSummary:
+    estimates: tuple
+    mean_value: float
+    mean_variance: float
+    empirical_variance: float
+
+    @property
+    def reps(self) -> int:
+        return len(self.estimates)
+
+    @property
+    def values(self) -> np.ndarray:
+        return np.array([e.value for e in self.estimates])
+
+    @property
+    def variances(self) -> np.ndarray:
+        return np.array([e.variance for e in self.estimates])
+
+
+# ---------------------------------------------------------------------------
+class PhiloxStream:
+    """Host view of the engine's stream (seed, stratum, rep): uniforms in
+    [0, 1) with 32-bit resolution, word w of draw i = block w//4, lane w%4.
+    Mirrors mc_stream's role (mc.py:92-95) for inspection and tests; the
+    estimators draw on the GPU."""
+
+    def __init__(self, seed: int, stratum: int = 0, rep: int = 0):
+        self.seed, self.stratum, self.rep = int(seed), int(stratum), int(rep)
+        self._draw = 0
+
+    def words(self, draw: int, count: int) -> np.ndarray:
+        key = (ctypes.c_uint32 * 2)(self.seed & 0xFFFFFFFF, self.seed >> 32)
+        out = np.empty(count, dtype=np.uint32)
+        blk = (ctypes.c_uint32 * 4)()
+        for j in range((count + 3) // 4):
+            ctr = (ctypes.c_uint32 * 4)(j, draw, self.stratum, self.rep)
+            _native.lib().bp_philox4x32_10(ctr, key, blk)
+            n = min(4, count - 4 * j)
+            out[4 * j:4 * j + n] = list(blk)[:n]
+        return out
+
+    def bits(self, probs: np.ndarray) -> np.ndarray:
+        """Next draw's Bernoulli bits, bit t up with probability probs[t]."""
+        probs = np.asarray(probs, dtype=np.float64)
+        w = self.words(self._draw, probs.shape[0]).astype(np.uint64)
+        self._draw += 1
+        thr = np.where(probs >= 1.0, np.uint64(1 << 32), np.floor(np.clip(probs, 0.0, 1.0) * 4294967296.0)
+                       .astype(np.uint64))
+        return w < thr
+
+    def random(self, size: int) -> np.ndarray:
+        """Uniforms of one draw's words (32-bit resolution)."""
+        w = self.words(self._draw, int(size))
+        self._draw += 1
+        return w.astype(np.float64) / 4294967296.0
+
+
+def mc_stream(seed: int, stratum: int = 0, rep: int = 0) -> PhiloxStream:
+    return PhiloxStream(seed, stratum, rep)
+
+
+def sample_path(params, rng: PhiloxStream) -> BernoulliPath:
+    bits = rng.bits(params.up_probs)
+    return BernoulliPath.from_bits([int(b) for b in bits])
+
+
+# ---------------------------------------------------------------------------
+def _discount(req) -> float:
+    return math.exp(-req.inputs.q * req.inputs.T)
+
+
+def _device(req) -> int:
+    devs = getattr(req, "devices", None)
+    if devs:
+        return int(devs[0])
+    import os
+    env = os.environ.get("BINPATHS_DEVICES", "").strip()
+    return int(env.split(",")[0]) if env else 0
+
+
+def _tree(req):
+    from .exact import tree_of
+    return tree_of(req)
+
+
+def _stratified_partition(req, M: int) -> PathPartition:
+    if M & (M - 1) != 0:
+        raise InvalidWorkerCount(f"stratum count must be a power of two, got {M}")
+    n = int(req.inputs.N)
+    if n > 62:  # MC only: 63/64-step paths (BASELINE config 4), prefix strata as in make_partition
+        r = M.bit_length() - 1
+        if r > n:
+            raise InvalidWorkerCount(f"stratum count {M} exceeds the paths of an {n}-step tree")
+        return PathPartition(n=n, m=M, prefix_width=r, blocks=tuple((i,) for i in range(M)))
+    return make_partition(n, M)
+
+
+def _strata_stats(req, r: int, draws, seed: int, rep0: int, n_reps: int):
+    """(theta[n_reps, M], sse[n_reps, M], kernel_ms) from the GPU."""
+    tree, keep = _tree(req)
+    M = 1 << r
+    d = np.ascontiguousarray(draws, dtype=np.uint64)
+    theta = np.zeros(n_reps * M)
+    sse = np.zeros(n_reps * M)
+    ms = ctypes.c_double()
+    _native.check(_native.lib().bp_mc_strata(ctypes.byref(tree), 1 << kind_bit(req.kind), r, _native.u64ptr(d),
+                                             seed, rep0, n_reps, _device(req), _native.dptr(theta),
+                                             _native.dptr(sse), ctypes.byref(ms)))
+    del keep
+    return theta.reshape(n_reps, M), sse.reshape(n_reps, M), ms.value
+
+
+def allocate_strata(partition: PathPartition, params, R: int) -> list:
+    """Largest-remainder split of R draws proportional to stratum mass,
+    >= 1 draw for every positive-mass stratum, ties to the lower rank
+    (mc.py:162-194)."""
+    masses = [block_probability(params, partition, m) for m in range(partition.m)]
+    positive = [m for m in range(partition.m) if masses[m] > 0.0]
+    if R < len(positive):
+        raise InfeasibleAllocation(f"R={R} draws cannot cover {len(positive)} strata with positive mass")
+    targets = [R * w for w in masses]
+    alloc = [int(math.floor(t)) for t in targets]
+    order = sorted(range(partition.m), key=lambda m: (alloc[m] - targets[m], m))
+    for m in order[: R - sum(alloc)]:
+        alloc[m] += 1
+    floor_of = [1 if w > 0.0 else 0 for w in masses]
+    while True:
+        starved = next((m for m in positive if alloc[m] == 0), None)
+        if starved is None:
+            return alloc
+        donor = max(range(partition.m), key=lambda m: (alloc[m] - floor_of[m], -m))
+        alloc[donor] -= 1
+        alloc[starved] += 1
+
+
+def _basic_from(req, cfg, theta, sse) -> Estimate:
+    disc = _discount(req)
+    variance = disc * disc * (sse / (cfg.R * cfg.R))
+    return Estimate(value=disc * theta, variance=variance, std_error=math.sqrt(variance), R_used=cfg.R,
+                    method="basic", seed=cfg.seed)
+
+
+def _partitioned_from(req, cfg, masses, alloc, thetas, sses, equal: bool) -> Estimate:
+    disc = _discount(req)
+    w = np.asarray(masses, dtype=np.float64)
+    th = np.asarray(thetas, dtype=np.float64)
+    if equal:
+        var_theta = float(np.sum(w * w * np.asarray(sses) / (cfg.R * cfg.R)))
+    else:
+        var_theta = float(np.sum(np.asarray(sses))) / (cfg.R * cfg.R)
+    variance = disc * disc * var_theta
+    return Estimate(value=disc * float(np.sum(th * w)), variance=variance, std_error=math.sqrt(variance),
+                    R_used=int(sum(alloc)), method="partitioned", seed=cfg.seed,
+                    per_stratum=tuple((m, int(alloc[m]), float(th[m])) for m in range(len(alloc))))
+
+
+def _basic_reps(req, cfg, rep0, n_reps):
+    if cfg.R < 2:
+        raise InvalidInput(f"basic estimator needs R >= 2, got {cfg.R}")
+    theta, sse, _ = _strata_stats(req, 0, [cfg.R], cfg.seed, rep0, n_reps)
+    return [_basic_from(req, cfg, float(theta[k, 0]), float(sse[k, 0])) for k in range(n_reps)]
+
+
+def _partitioned_reps(req, cfg, rep0, n_reps):
+    if cfg.R < cfg.M:
+        raise InfeasibleAllocation(f"partitioned estimator needs R >= M, got R={cfg.R}, M={cfg.M}")
+    part = _stratified_partition(req, cfg.M)
+    masses = [block_probability(req.params, part, m) for m in range(cfg.M)]
+    alloc = allocate_strata(part, req.params, cfg.R)
+    theta, sse, _ = _strata_stats(req, part.prefix_width, alloc, cfg.seed, rep0, n_reps)
+    return [_partitioned_from(req, cfg, masses, alloc, theta[k], sse[k], equal=False) for k in range(n_reps)]
+
+
+def _equal_reps(req, cfg, rep0, n_reps):
+    part = _stratified_partition(req, cfg.M)
+    masses = [block_probability(req.params, part, m) for m in range(cfg.M)]
+    alloc = [cfg.R] * cfg.M
+    theta, sse, _ = _strata_stats(req, part.prefix_width, alloc, cfg.seed, rep0, n_reps)
+    return [_partitioned_from(req, cfg, masses, alloc, theta[k], sse[k], equal=True) for k in range(n_reps)]
+
+
+def _shared_reps(req, cfg, rep0, n_reps):
+    if cfg.R < 2:
+        raise InvalidInput(f"shared estimator needs R >= 2, got {cfg.R}")
+    part = _stratified_partition(req, cfg.M)
+    masses = np.array([block_probability(req.params, part, m) for m in range(cfg.M)])
+    tree, keep = _tree(req)
+    im = np.zeros(n_reps)
+    isse = np.zeros(n_reps)
+    sm = np.zeros(n_reps * cfg.M)
+    ms = ctypes.c_double()
+    _native.check(_native.lib().bp_mc_shared(ctypes.byref(tree), 1 << kind_bit(req.kind), part.prefix_width, cfg.R,
+                                             _native.dptr(masses), cfg.seed, rep0, n_reps, _device(req),
+                                             _native.dptr(im), _native.dptr(isse), _native.dptr(sm),
+                                             ctypes.byref(ms)))
+    del keep
+    sm = sm.reshape(n_reps, cfg.M)
+    disc = _discount(req)
+    out = []
+    for k in range(n_reps):
+        variance = disc * disc * (float(isse[k]) / (cfg.R * cfg.R))
+        out.append(Estimate(value=disc * float(im[k]), variance=variance, std_error=math.sqrt(variance),
+                            R_used=cfg.R, method="shared", seed=cfg.seed,
+                            per_stratum=tuple((m, cfg.R, float(sm[k, m])) for m in range(cfg.M))))
+    return out
+
+
+def estimate_basic(req, cfg: McConfig, rep: int = 0) -> Estimate:
+    """Plain MC: R i.i.d. paths on stream (seed, 0, rep) (mc.py:135-159)."""
+    return _basic_reps(req, cfg, rep, 1)[0]
+
+
+def estimate_partitioned(req, cfg: McConfig, rep: int = 0, eval_threads: int = 1) -> Estimate:
+    """Stratified MC, proportional allocation (mc.py:234-257).  eval_threads
+    is accepted for API parity; results never depend on it."""
+    return _partitioned_reps(req, cfg, rep, 1)[0]
+
+
+def estimate_partitioned_equal(req, cfg: McConfig, rep: int = 0, eval_threads: int = 1) -> Estimate:
+    """Stratified MC, R draws in every stratum (mc.py:260-284)."""
+    return _equal_reps(req, cfg, rep, 1)[0]
+
+
+def estimate_shared(req, cfg: McConfig, rep: int = 0, eval_threads: int = 1) -> Estimate:
+    """Shared-sample MC: one suffix sample under every prefix (mc.py:287-331)."""
+    return _shared_reps(req, cfg, rep, 1)[0]
+
+
+_BATCHED = {
+    estimate_basic: _basic_reps,
+    estimate_partitioned: _partitioned_reps,
+    estimate_partitioned_equal: _equal_reps,
+    estimate_shared: _shared_reps,
+}
+
+
+def run_repetitions(estimator: Callable, req, cfg: McConfig, **estimator_kwargs) -> RepetitionSummary:
+    """cfg.reps repetitions keyed by rep = 0..reps-1 (mc.py:334-353).
+
+    For this package's estimators all repetitions run in ONE launch (the rep
+    index is part of the Philox counter); the estimates are bit-identical to
+    calling the estimator once per rep.
+    """
+    batched = _BATCHED.get(estimator)
+    if batched is not None:
+        estimates = tuple(batched(req, cfg, 0, cfg.reps))
+    else:
+        estimates = tuple(estimator(req, cfg, rep=k, **estimator_kwargs) for k in range(cfg.reps))
+    values = np.array([e.value for e in estimates])
+    variances = np.array([e.variance for e in estimates])
+    return RepetitionSummary(estimates=estimates, mean_value=float(values.mean()),
+                             mean_variance=float(variances.mean()),
+                             empirical_variance=float(np.var(values, ddof=1)) if len(estimates) > 1 else 0.0)
