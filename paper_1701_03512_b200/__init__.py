@@ -19,7 +19,7 @@ from .payoffs import (ASIAN_CALL, FLOATING_LOOKBACK, GpuPayoff, PayoffKind, kind
 from .mc import (Estimate, McConfig, PhiloxStream, RepetitionSummary, allocate_strata, estimate_basic,
                  estimate_partitioned, estimate_partitioned_equal, estimate_shared, mc_stream, run_repetitions,
                  sample_path)
-from .exact import (LARGE_DEPTH, ExactResult, ValuationRequest, value_exact, value_exact_parallel,
-                    value_exact_serial, value_leaf_formula)
+from .exact import (LARGE_DEPTH, ExactResult, ValuationRequest, price_batch, value_exact, value_exact_batch,
+                    value_exact_parallel, value_exact_serial, value_leaf_formula)
 
 __version__ = "0.1.0"

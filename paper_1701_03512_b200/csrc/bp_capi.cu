@@ -750,3 +750,59 @@ extern "C" int bp_mc_shared(const bp_tree* tree, uint32_t payoff, int r, uint64_
   if (kernel_ms) *kernel_ms = ms;
   return BP_OK;
 }
+
+// ---------------------------------------------------------------------------
+// batched exact pricing (K3)
+extern "C" int bp_exact_batch(const bp_tree* trees, int n_opts, uint32_t payoff, int device, double* values,
+                              double* kernel_ms) {
+  if (!trees || n_opts < 1 || !values) return fail(BP_E_INVALID_INPUT, "bad batch arguments");
+  unsigned kind;
+  int rc = single_kind(payoff, &kind);
+  if (rc) return rc;
+  const int N = trees[0].n_steps;
+  if (N < kFastMinN || N > 40) return fail(BP_E_INVALID_INPUT, "batched pricing supports 16 <= N <= 40");
+  std::vector<BatchOption> h(n_opts);
+  for (int i = 0; i < n_opts; ++i) {
+    const bp_tree* t = &trees[i];
+    if ((rc = validate_tree(t, 62))) return rc;
+    if (t->n_steps != N) return fail(BP_E_LENGTH_MISMATCH, "all trees of a batch must have the same N");
+    if (!constant_p(t)) return fail(BP_E_NONCONSTANT_PROBS, "batched pricing needs a constant up probability");
+    if (!(t->u > t->d)) return fail(BP_E_INVALID_INPUT, "batched pricing needs u > d");
+    h[i] = BatchOption{t->S0, t->K, t->u, t->d, t->up_probs[0], t->disc};
+  }
+  if (device < 0 || device >= bp_device_count()) return fail(BP_E_NO_DEVICE, "no CUDA device " + std::to_string(device));
+  BP_CUDA(cudaSetDevice(device));
+  keep_pool(device);
+  cudaStream_t st;
+  BP_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  struct StreamGuard {
+    cudaStream_t s;
+    ~StreamGuard() {
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    }
+  } sg{st};
+  const int cpo = batch_ctas_per_option(n_opts);
+  DevBuf<BatchOption> d_o;
+  DevBuf<double> d_v;
+  DevBuf<double2> d_p;
+  d_o.st = d_v.st = d_p.st = st;
+  BP_CUDA(cudaMallocAsync((void**)&d_o.p, sizeof(BatchOption) * n_opts, st));
+  BP_CUDA(cudaMallocAsync((void**)&d_v.p, sizeof(double) * n_opts, st));
+  BP_CUDA(cudaMallocAsync((void**)&d_p.p, sizeof(double2) * ((size_t)n_opts << cpo), st));
+  BP_CUDA(cudaMemcpyAsync(d_o.p, h.data(), sizeof(BatchOption) * n_opts, cudaMemcpyHostToDevice, st));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, st);
+  BP_CUDA(launch_exact_batch(d_o.p, n_opts, N, kind, d_v.p, d_p.p, cpo, st));
+  cudaEventRecord(e1, st);
+  BP_CUDA(cudaMemcpyAsync(values, d_v.p, sizeof(double) * n_opts, cudaMemcpyDeviceToHost, st));
+  BP_CUDA(cudaStreamSynchronize(st));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (kernel_ms) *kernel_ms = ms;
+  return BP_OK;
+}

@@ -26,8 +26,8 @@ struct BatchOption {
   double S0, K, u, d, p, disc;
 };
 cudaError_t launch_exact_batch(const BatchOption* opts_dev, int n_opts, int N, unsigned kind, double* values_dev,
-                               double2* scratch_dev, int ctas_per_option, cudaStream_t st);
-int batch_ctas_per_option(int N);
+                               double2* scratch_dev, int cpo_log2, cudaStream_t st);
+int batch_ctas_per_option(int n_opts);  // log2 of CTAs per option
 
 // Monte Carlo, see bp_mc_kernels.cu
 struct McArgs {

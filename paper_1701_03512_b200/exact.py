@@ -169,3 +169,42 @@ def value_leaf_formula(req) -> float:
         weights = np.exp(logc + j * math.log(p) + (n - j) * math.log1p(-p))
     values = terminal_payoff(req.kind, leaf_prices(req.params, req.inputs.S0), req.inputs.K)
     return math.exp(-req.inputs.q * req.inputs.T) * float(np.dot(weights, values))
+
+
+def price_batch(N: int, S0, K, u, d, p, disc, kind, device: int = 0, with_time: bool = False):
+    """Exact values of many independent trees (arrays, same N), one kind,
+    one launch (bp_exact_batch).  Returns a numpy array (and kernel ms)."""
+    arrs = np.broadcast_arrays(*(np.asarray(x, dtype=np.float64) for x in (S0, K, u, d, p, disc)))
+    n = arrs[0].size
+    S0a, Ka, ua, da, pa, da_ = (np.ascontiguousarray(a.reshape(-1)) for a in arrs)
+    probs = np.ascontiguousarray(np.repeat(pa[:, None], N, axis=1))
+    trees = (_native.BpTree * n)()
+    for i in range(n):
+        trees[i] = _native.BpTree(int(N), 0, S0a[i], Ka[i], ua[i], da[i], da_[i],
+                                  probs[i].ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+    out = np.zeros(n)
+    ms = ctypes.c_double()
+    _native.check(_native.lib().bp_exact_batch(trees, n, 1 << kind_bit(kind), int(device), _native.dptr(out),
+                                               ctypes.byref(ms)))
+    return (out, ms.value) if with_time else out
+
+
+def value_exact_batch(reqs: Sequence, kind=None, device: Optional[int] = None) -> np.ndarray:
+    """value_exact_parallel over a list of requests (same N, constant p) in
+    one launch.  Returns the values in request order."""
+    reqs = list(reqs)
+    if not reqs:
+        return np.zeros(0)
+    kind = reqs[0].kind if kind is None else kind
+    N = int(reqs[0].inputs.N)
+    for r in reqs:
+        _check_enumerable(r)
+        if int(r.inputs.N) != N:
+            raise LengthMismatch("all requests of a batch must share N")
+        if r.params.constant_up_prob() is None:
+            raise NonConstantProbs("batched pricing needs one constant up probability per tree")
+    cols = [(float(r.inputs.S0), float(r.inputs.K), float(r.params.u), float(r.params.d),
+             float(r.params.up_probs[0]), math.exp(-float(r.inputs.q) * float(r.inputs.T))) for r in reqs]
+    S0, K, u, d, p, disc = (np.array(c) for c in zip(*cols))
+    dev = _devices(reqs[0])[0] if device is None else device
+    return price_batch(N, S0, K, u, d, p, disc, kind, device=dev)
