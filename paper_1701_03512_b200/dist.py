@@ -64,9 +64,9 @@ def gather_partials(local, world: int, group=None):
     import torch
     import torch.distributed as dist
 
-    out = torch.empty((world,) + tuple(local.shape), dtype=local.dtype, device=local.device)
+    out = torch.empty((world * local.shape[0],) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
     dist.all_gather_into_tensor(out, local.contiguous(), group=group)
-    return out.reshape((-1,) + tuple(local.shape[1:]))
+    return out
 
 
 class ShardedExact:

@@ -92,3 +92,68 @@ def test_drop_in_entry_points():
         v = bp.value_exact_parallel(req)
         assert v == bp.value_exact_serial(req)
         assert _close(v, g["asian_call"])
+
+
+def test_config2_golden_N30_two_payoffs_one_pass():
+    g = load_golden("exact_config2.json")
+    req = _req(30, 100.0, g["K"], 0.05, 1.0, g["u"], g["d"], g["p"])
+    res = bp.value_exact(req, kinds=[bp.ASIAN_CALL, bp.FLOATING_LOOKBACK])
+    assert res.engine == "affine-threshold"
+    assert _close(res.values["asian-call"], g["asian_call"]), (res.values, g["asian_call"])
+    assert _close(res.values["float-lookback"], g["float_lookback"]), (res.values, g["float_lookback"])
+
+
+@pytest.mark.parametrize("N", [20, 30])
+def test_superblock_sharding_is_bitwise_invariant_across_G(N):
+    """Emulate G = 1, 2, 4, 8 ranks on one GPU: every rank's super-block range
+    is enqueued separately (bp_exact_superblocks) and the gathered partials
+    are combined in fixed order -- identical bits for every G."""
+    import torch
+    from paper_1701_03512_b200 import dist as bpd
+    from paper_1701_03512_b200.exact import tree_of
+    P = bp.classic_crr(N, 0.2, 0.05, 1.0)
+    req = _req(N, 100.0, 103.0, 0.05, 1.0, P.u, P.d, P.up_probs[0])
+    tree, keep = tree_of(req)
+    mask = (1 << 4) | (1 << 5)
+    results = {}
+    for G in (1, 2, 4, 8):
+        parts = []
+        for rank in range(G):
+            sh = bpd.ShardedExact(tree, keep, mask, rank, G, 0)
+            sh.enqueue()
+            torch.cuda.synchronize()
+            parts.append(sh.local.cpu().numpy())
+        results[G] = bpd.combine(np.concatenate(parts), mask)
+    assert results[1] == results[2] == results[4] == results[8]
+    single = bp.value_exact(req, kinds=[bp.ASIAN_CALL, bp.FLOATING_LOOKBACK])
+    assert single.values == results[1]
+    # the in-process multi-device path (one host thread per listed device)
+    twin = bp.value_exact(req, kinds=[bp.ASIAN_CALL, bp.FLOATING_LOOKBACK], devices=[0, 0, 0, 0])
+    assert twin.values == results[1] and twin.n_devices == 4
+
+
+def test_bookkeeping_code_checksum_large_N():
+    P = bp.classic_crr(28, 0.2, 0.05, 1.0)
+    req = _req(28, 100.0, 100.0, 0.05, 1.0, P.u, P.d, P.up_probs[0])
+    res = bp.value_exact(req, kinds=[bp.ASIAN_CALL], count=True)
+    N = 28
+    assert res.leaves == 1 << N
+    assert res.code_sum == ((1 << (N - 1)) * ((1 << N) - 1)) % (1 << 64)
+    assert [int(x) for x in res.hist] == [math.comb(N, h) for h in range(N + 1)]
+
+
+def test_guard_and_extreme_lattices():
+    # guard fires before the launch
+    P = bp.classic_crr(30, 0.2, 0.05, 1.0)
+    with pytest.raises(bp.EnumerationGuard):
+        bp.value_exact_serial(_req(30, 100.0, 100.0, 0.05, 1.0, P.u, P.d, P.up_probs[0], force=False))
+    # heavy-tailed beta-CRR desk (sigma = 3): fast engine vs path walk
+    inputs = bp.MarketInputs(S0=20.0, K=100.0, q=0.06, sigma=3.0, T=1.0, N=18)
+    D = bp.derive_crr(inputs)
+    req = bp.ValuationRequest(inputs=inputs, params=D, kind=bp.PayoffKind.ASIAN_PUT)
+    kinds = [bp.resolve_kind(k) for k in ALL]
+    a = bp.value_exact(req, kinds=kinds)
+    b = bp.value_exact(req, kinds=kinds, generic=True)
+    assert a.engine == "affine-threshold"
+    for k in ALL:
+        assert _close(a.values[k], b.values[k]), (k, a.values[k], b.values[k])
