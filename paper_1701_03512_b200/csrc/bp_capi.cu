@@ -9,6 +9,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -89,13 +90,15 @@ static bool constant_p(const bp_tree* t) {
 // ---------------------------------------------------------------------------
 // layout: a pure function of (N, engine) so every device count and every
 // machine uses the same decomposition (bitwise reproducibility across G).
-static const int kFastL = 8;
-
-struct TableSet {
-  std::vector<double> t[3];  // c, mx, mn  (unscaled), 2^L
-  double scale_up[3], scale_dn[3];
-  bool ok[3];
-};
+// inner block bits of the fast engine (8 or 9; BINPATHS_INNER_BITS overrides)
+static int fast_L() {
+  static int L = [] {
+    const char* e = std::getenv("BINPATHS_INNER_BITS");
+    const int v = e ? std::atoi(e) : 8;
+    return (v == 8 || v == 9) ? v : 8;
+  }();
+  return L;
+}
 
 static void build_inner(int L, double u, double d, std::vector<double>& c, std::vector<double>& mx,
                         std::vector<double>& mn, std::vector<double>& e, std::vector<int>& h) {
@@ -124,27 +127,6 @@ static void build_inner(int L, double u, double d, std::vector<double>& c, std::
   }
 }
 
-// a = 1 - e where min = f 2^e, f in [0.5, 1): scaled min in [1, 2)
-static bool table_scale(const std::vector<double>& t, double& up, double& dn) {
-  double mn = INFINITY, mxv = 0.0;
-  for (double v : t) {
-    mn = std::min(mn, v);
-    mxv = std::max(mxv, v);
-  }
-  if (!(mn > 0.0) || !std::isfinite(mxv)) return false;
-  int e = 0;
-  std::frexp(mn, &e);
-  const int a = 1 - e;
-  if (a < -(1023 - kMaskExp) + 0 || a > 1000) return false;  // 2^(1007-a) must be finite
-  if (kMaskExp - a > 1023) return false;
-  up = std::ldexp(1.0, a);
-  dn = std::ldexp(1.0, kMaskExp - a);
-  if (!std::isfinite(mxv * up) || mxv * up > 1e300) return false;
-  return true;
-}
-
-static int ilog2_floor(unsigned long long x) { return 63 - __builtin_clzll(x); }
-
 static Layout choose_layout(const bp_tree* t, uint32_t payoffs, uint32_t flags, bool* fast_possible) {
   const int N = t->n_steps;
   Layout lay{};
@@ -161,15 +143,15 @@ static Layout choose_layout(const bp_tree* t, uint32_t payoffs, uint32_t flags, 
   if (fast) {
     std::vector<double> c, mx, mn, e;
     std::vector<int> h;
-    build_inner(kFastL, t->u, t->d, c, mx, mn, e, h);
-    double up, dn;
-    if (!table_scale(c, up, dn) || !table_scale(mx, up, dn) || !table_scale(mn, up, dn)) fast = false;
+    build_inner(fast_L(), t->u, t->d, c, mx, mn, e, h);
+    for (double v : c)
+      if (!std::isfinite(v)) fast = false;
   }
   if (fast_possible) *fast_possible = fast;
   if (fast) {
     lay.engine = 1;
-    lay.L = kFastL;
-    lay.D = N - kFastL;
+    lay.L = fast_L();
+    lay.D = N - lay.L;
     const int free_bits = lay.D - 5;  // bits above the lane
     lay.m = std::max(0, std::min(6, free_bits - kUnitTargetLog2));
     lay.Dp = lay.D - lay.m;
@@ -191,27 +173,56 @@ static Layout choose_layout(const bp_tree* t, uint32_t payoffs, uint32_t flags, 
   return lay;
 }
 
-static int build_fast_args(const bp_tree* t, const Layout& lay, unsigned km, std::vector<unsigned char>& buf) {
-  const int L = lay.L;
-  if (L != 8) return fail(BP_E_INVALID_INPUT, "unsupported inner block size");
-  buf.assign(exact_args_size(L), 0);
-  ExactArgs<8>& a = *reinterpret_cast<ExactArgs<8>*>(buf.data());
+// Inner table of one kind, laid out by position: class-major, sorted inside a
+// class in the kind's compare direction (descending for '>' kinds AC / FL,
+// ascending for '<' kinds AP / FLP), plus the group prefix sums.
+template <int L>
+static void kind_table_layout(int kind, const std::vector<double>& c, const std::vector<double>& mx,
+                              const std::vector<double>& mn, double* pos_out /* 2^L */,
+                              double (*gpre)[kGroupSlots] /* n_groups(L) */) {
+  const std::vector<double>& v = (kind == kAC || kind == kAP) ? c : (kind == kFL) ? mx : mn;
+  const bool desc = (kind == kAC || kind == kFL);
+  for (int cl = 0; cl <= L; ++cl) {
+    std::vector<double> cls;
+    for (int s = 0; s < (1 << L); ++s)
+      if (__builtin_popcount((unsigned)s) == cl) cls.push_back(v[s]);
+    if (desc)
+      std::sort(cls.begin(), cls.end(), [](double a, double b) { return a > b; });
+    else
+      std::sort(cls.begin(), cls.end());
+    const int start = class_start(L, cl);
+    for (size_t i = 0; i < cls.size(); ++i) pos_out[start + i] = cls[i];
+    for (int g = 0; g < class_groups(L, cl); ++g) {
+      double* P = gpre[group_base(L, cl) + g];
+      const int len = std::min<int>(8, (int)cls.size() - 8 * g);
+      double sum = 0.0, comp = 0.0;  // compensated prefix sums, rounded once
+      P[0] = 0.0;
+      for (int n = 1; n < kGroupSlots; ++n) {
+        if (n <= len) comp_add(sum, comp, cls[8 * g + n - 1]);
+        P[n] = sum + comp;
+      }
+    }
+  }
+}
+
+template <int L>
+static int fill_fast_args(const bp_tree* t, const Layout& lay, unsigned km, std::vector<unsigned char>& buf) {
+  buf.assign(sizeof(ExactArgs<L>), 0);
+  ExactArgs<L>& a = *reinterpret_cast<ExactArgs<L>*>(buf.data());
   std::vector<double> c, mx, mn, e;
   std::vector<int> h;
   build_inner(L, t->u, t->d, c, mx, mn, e, h);
-  const std::vector<double>* tabs[3] = {&c, &mx, &mn};
-  double up[3] = {1, 1, 1}, dn[3] = {1, 1, 1};
-  for (int i = 0; i < 3; ++i)
-    if (!table_scale(*tabs[i], up[i], dn[i])) return fail(BP_E_INVALID_INPUT, "lattice outside the fast engine range");
-  // tables in use: one -> tab[s]; two -> interleaved tab[2s + slot]
-  std::vector<int> use;
-  if (km & ((1u << kAC) | (1u << kAP))) use.push_back(0);
-  if (km & (1u << kFL)) use.push_back(1);
-  if (km & (1u << kFLP)) use.push_back(2);
-  if (use.size() > 2) return fail(BP_E_INVALID_INPUT, "more than two inner tables requested in one launch");
-  const int nt = (int)use.size();
-  for (int slot = 0; slot < nt; ++slot)
-    for (int s = 0; s < (1 << L); ++s) a.tab[nt == 1 ? s : 2 * s + slot] = (*tabs[use[slot]])[s] * up[use[slot]];
+  // table slots in kind order AC, AP, FL, FLP (must match k_exact_fast)
+  std::vector<int> kinds;
+  for (int k : {kAC, kAP, kFL, kFLP})
+    if ((km >> k) & 1) kinds.push_back(k);
+  if (kinds.size() > 2) return fail(BP_E_INVALID_INPUT, "more than two inner tables requested in one launch");
+  const int nt = (int)kinds.size();
+  std::vector<double> pos(1 << L);
+  for (int slot = 0; slot < nt; ++slot) {
+    kind_table_layout<L>(kinds[slot], c, mx, mn, pos.data(), a.gpre[slot]);
+    for (int i = 0; i < (1 << L); ++i) a.tab[slot * (1 << L) + i] = pos[i];
+  }
   // middle tables (chunk of m steps)
   const int m = lay.m;
   std::vector<double> mc, mmx, mmn, me;
@@ -242,9 +253,7 @@ static int build_fast_args(const bp_tree* t, const Layout& lay, unsigned km, std
     for (int j = 0; j < cc; ++j) r *= t->u;
     for (int j = cc; j < L; ++j) r *= t->d;
     a.e_cls[cc] = r;
-    double b = 1.0;
-    for (int j = 0; j < cc; ++j) b = b * (L - j) / (j + 1);
-    a.b_cls[cc] = std::round(b);
+    a.b_cls[cc] = (double)binom(L, cc);
   }
   ExactScalars& s = a.s;
   s.S0 = t->S0;
@@ -253,10 +262,6 @@ static int build_fast_args(const bp_tree* t, const Layout& lay, unsigned km, std
   s.u = t->u;
   s.d = t->d;
   s.invN = 1.0 / N;
-  for (int i = 0; i < 3; ++i) {
-    s.sc_up[i] = up[i];
-    s.sc_dn[i] = dn[i];
-  }
   s.N = N;
   s.L = L;
   s.D = lay.D;
@@ -266,6 +271,21 @@ static int build_fast_args(const bp_tree* t, const Layout& lay, unsigned km, std
   s.q = lay.q;
   s.zero = 0;
   return BP_OK;
+}
+
+static int build_fast_args(const bp_tree* t, const Layout& lay, unsigned km, std::vector<unsigned char>& buf) {
+  switch (lay.L) {
+    case 8: return fill_fast_args<8>(t, lay, km, buf);
+    case 9: return fill_fast_args<9>(t, lay, km, buf);
+    default: return fail(BP_E_INVALID_INPUT, "unsupported inner block size");
+  }
+}
+
+static void set_units(std::vector<unsigned char>& buf, int L, unsigned long long u0, unsigned long long u1) {
+  ExactScalars* s = (L == 8) ? &reinterpret_cast<ExactArgs<8>*>(buf.data())->s
+                             : &reinterpret_cast<ExactArgs<9>*>(buf.data())->s;
+  s->unit_first = u0;
+  s->unit_end = u1;
 }
 
 // the groups of kinds launched together in the fast engine
@@ -332,9 +352,7 @@ static int enqueue_superblocks(const bp_tree* t, uint32_t payoffs, uint32_t flag
       std::vector<unsigned char> buf;
       int rc = build_fast_args(t, lay, km, buf);
       if (rc) return rc;
-      ExactArgs<8>& a = *reinterpret_cast<ExactArgs<8>*>(buf.data());
-      a.s.unit_first = u0;
-      a.s.unit_end = u1;
+      set_units(buf, lay.L, u0, u1);
       const int occ = std::max(1, occupancy_exact_fast(lay.L, km, cnt_g));
       const unsigned long long want = (n_units + 7) / 8;
       const int grid = (int)std::max<unsigned long long>(1, std::min<unsigned long long>(want, (unsigned long long)occ * sms));

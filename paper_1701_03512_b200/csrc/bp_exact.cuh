@@ -15,19 +15,22 @@
 // * the thread walks its prefix once (S, running sum, max, min, up count),
 //   then visits its 2^m nodes with the middle tables (mid_*), then every
 //   leaf of each node in a fully unrolled block of 2^L leaves;
-// * every leaf is evaluated explicitly, but the affine structure of the
-//   payoffs turns the per-leaf work into ONE compare and ONE masked FMA:
+// * every leaf is evaluated explicitly with ONE compare; the affine structure
+//   of the payoffs makes the compare the whole payoff decision:
 //     Asian:    sum_j S_j = Sig_node + S_node * c_s   (c_s = sum of the L
 //               relative prices of inner suffix s, a table)
 //     lookback: max_j S_j = max(Mx_node, S_node * mx_s)
-//   so "payoff > 0" is "c_s > theta_node" with theta = (N K - Sig)/S, and the
-//   leaf contributes S c_s + (Sig - N K).  Per up-count class c = |s| the
-//   block accumulates A_c = sum of c_s over in-the-money leaves and their
-//   count n_c; the node value is sum_c w[h + c] (S A_c + base n_c) with
-//   w[h] = e^{-qT} p^h (1-p)^{N-h} (exact.py:95,99 folded into one table).
-// * per-unit compensated partials -> fixed-order super-block reduce ->
-//   fixed-order combination of the (at most 8) super-blocks, so the result
-//   is bitwise independent of the number of GPUs that computed it.
+//   so "payoff > 0" is "c_s > theta_node" with theta = (N K - Sig)/S, and an
+//   in-the-money leaf contributes S c_s + (Sig - N K).
+// * the inner table is laid out by up-count class c = |s| and, inside a
+//   class, sorted in the compare direction (host side, per tree), then cut
+//   into groups of <= 8 positions.  Inside a group the in-the-money leaves
+//   are therefore a prefix: the per-leaf compares (DSETP + predicated
+//   increment) give the count n, and the group's contribution sum_ITM c_s
+//   is the precomputed prefix sum P_g[n] (one shared-memory load per group).
+//   Per class the node keeps A_c = sum of ITM values and n_c = ITM count;
+//   the node value is sum_c w[h + c] (S A_c + base n_c), w[h] =
+//   e^{-qT} p^h (1-p)^{N-h} (exact.py:95,99 folded into one table).
 #pragma once
 #include <cstdint>
 #include "bp_common.cuh"
@@ -60,11 +63,34 @@ struct ExactScalars {
   unsigned long long unit_first, unit_end;
 };
 
+// binomial coefficients and the class / group layout of the inner block
+// (iterative constexpr: usable in templates, host and device code)
+__host__ __device__ constexpr int binom(int n, int k) {
+  if (k < 0 || k > n) return 0;
+  long long r = 1;
+  for (int i = 1; i <= k; ++i) r = r * (n - k + i) / i;
+  return (int)r;
+}
+__host__ __device__ constexpr int class_start(int L, int c) {
+  int s = 0;
+  for (int i = 0; i < c; ++i) s += binom(L, i);
+  return s;
+}
+__host__ __device__ constexpr int class_groups(int L, int c) { return (binom(L, c) + 7) / 8; }
+__host__ __device__ constexpr int group_base(int L, int c) {
+  int s = 0;
+  for (int i = 0; i < c; ++i) s += class_groups(L, i);
+  return s;
+}
+__host__ __device__ constexpr int n_groups(int L) { return group_base(L, L + 1); }
+constexpr int kGroupSlots = 9;  // prefix sums for n = 0..8
+
 template <int L>
 struct __align__(16) ExactArgs {
-  // scaled inner tables: one table -> tab[s]; two tables -> interleaved
-  // (tab[2s] = first, tab[2s+1] = second) so one 16-byte load feeds a leaf
+  // inner tables by position (class-major, sorted in the compare direction
+  // inside a class), slot-major: tab[slot * 2^L + i]
   double tab[2 << L];
+  double gpre[2][n_groups(L)][kGroupSlots];  // group prefix sums per slot
   double mid_c[kMidMax], mid_e[kMidMax], mid_mx[kMidMax], mid_mn[kMidMax];
   int mid_h[kMidMax];
   double w[kMaxN + 2];    // e^{-qT} p^h (1-p)^{N-h}, h = 0..N (zero padded)

@@ -7,32 +7,75 @@
 
 namespace bp {
 
-__device__ __forceinline__ double u32_to_double(unsigned x) {
-  // exact: 2^52 + x - 2^52
-  return __hiloint2double(0x43300000, (int)x) - 4503599627370496.0;
+// ---------------------------------------------------------------------------
+// one explicit leaf test: n += (x OP th), as DSETP + predicated increment
+template <bool GT>
+__device__ __forceinline__ void leaf_test(int& n, double x, double th) {
+  if (GT)
+    asm("{.reg .pred p; setp.gt.f64 p, %1, %2; @p add.s32 %0, %0, 1;}" : "+r"(n) : "d"(x), "d"(th));
+  else
+    asm("{.reg .pred p; setp.lt.f64 p, %1, %2; @p add.s32 %0, %0, 1;}" : "+r"(n) : "d"(x), "d"(th));
 }
 
-// ---------------------------------------------------------------------------
+// The leaf block of one table slot: every position i of the 2^L inner
+// leaves is tested once; per group of <= 8 the ITM count n selects the
+// group's prefix sum.  acc[c] / cnt[c]: per-class ITM sum and count.
+// Compile-time recursion over (class C, group G) so every index is constant.
+template <int L, int NT, int SLOT, bool GT, int C, int G>
+struct LeafGroups {
+  static __device__ __forceinline__ void run(const double2* __restrict__ tb, const double* __restrict__ gpre, double th,
+                                             double (&acc)[L + 1], int (&cnt)[L + 1]) {
+    if constexpr (C <= L) {
+      constexpr int size = binom(L, C);
+      if constexpr (8 * G < size) {
+        constexpr int len = (size - 8 * G) < 8 ? (size - 8 * G) : 8;
+        constexpr int i0 = class_start(L, C) + 8 * G;
+        int n = 0;
+#pragma unroll
+        for (int j = 0; j < len; ++j) {
+          // 16-byte loads of positions (2k, 2k+1) of this slot's table
+          const int i = SLOT * (1 << L) + i0 + j;
+          const double2 v = tb[i >> 1];
+          const double x = (i & 1) ? v.y : v.x;
+          leaf_test<GT>(n, x, th);
+        }
+        acc[C] += gpre[(group_base(L, C) + G) * kGroupSlots + n];
+        cnt[C] += n;
+        LeafGroups<L, NT, SLOT, GT, C, G + 1>::run(tb, gpre, th, acc, cnt);
+      } else {
+        LeafGroups<L, NT, SLOT, GT, C + 1, 0>::run(tb, gpre, th, acc, cnt);
+      }
+    }
+  }
+};
+
+template <int L, int NT, int SLOT, bool GT>
+__device__ __forceinline__ void leaf_block(const double2* __restrict__ tb, const double* __restrict__ gpre, double th,
+                                           double (&acc)[L + 1], int (&cnt)[L + 1]) {
+  LeafGroups<L, NT, SLOT, GT, 0, 0>::run(tb, gpre, th, acc, cnt);
+}
+
 // K1: affine-threshold enumeration.  KM = compile-time kind mask.
 template <int L, unsigned KM, bool CNT>
 __global__ void __launch_bounds__(256)
 k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_out,
              unsigned long long* __restrict__ hist) {
-  constexpr int NL = 1 << L;
   constexpr int NC = L + 1;
+  constexpr int NG = n_groups(L);
   constexpr bool kAC_ = (KM >> kAC) & 1, kAP_ = (KM >> kAP) & 1, kFL_ = (KM >> kFL) & 1,
                  kFLP_ = (KM >> kFLP) & 1, kEC_ = (KM >> kEC) & 1, kEP_ = (KM >> kEP) & 1;
   constexpr bool needMx = kFL_, needMn = kFLP_;
+  // table slots in kind order AC, AP, FL, FLP
+  constexpr int NT = (int)kAC_ + (int)kAP_ + (int)kFL_ + (int)kFLP_;
+  static_assert(NT <= 2, "at most two tables per launch");
+  constexpr int slotAC = 0, slotAP = (int)kAC_, slotFL = (int)kAC_ + (int)kAP_, slotFLP = slotFL + (int)kFL_;
 
-  constexpr int NT_ = (int)(kAC_ || kAP_) + (int)kFL_ + (int)kFLP_;
   __shared__ double sw[kMaxN + 2 + NC];
   __shared__ unsigned long long shist[kMaxN + 2];
-  // two-table kernels read the interleaved tables from shared memory (one
-  // broadcast LDS.128 per leaf); one-table kernels read the constant bank
-  __shared__ __align__(16) double stab[NT_ == 2 ? (2 << L) : 2];
-  if (NT_ == 2)
-    for (int i = threadIdx.x; i < (2 << L); i += blockDim.x) stab[i] = a.tab[i];
+  __shared__ double sgpre[NT > 0 ? NT : 1][NG * kGroupSlots];
   for (int i = threadIdx.x; i < kMaxN + 2 + NC; i += blockDim.x) sw[i] = (i < kMaxN + 2) ? a.w[i] : 0.0;
+  for (int t = 0; t < NT; ++t)
+    for (int i = threadIdx.x; i < NG * kGroupSlots; i += blockDim.x) sgpre[t][i] = (&a.gpre[t][0][0])[i];
   if (CNT)
     for (int i = threadIdx.x; i < kMaxN + 2; i += blockDim.x) shist[i] = 0ull;
   __syncthreads();
@@ -41,7 +84,6 @@ k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_
   const int lane = threadIdx.x & 31;
   const unsigned long long warp_global = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5;
   const unsigned long long n_warps = (gridDim.x * (unsigned long long)blockDim.x) >> 5;
-  const int zlo = lane & sc.zero;
   const double INF = __longlong_as_double(0x7ff0000000000000ll);
   unsigned long long leaves = 0, code_sum = 0;
 
@@ -71,92 +113,42 @@ k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_
       const double Mnn = needMn ? fmin(Mn, S * a.mid_mn[j]) : 0.0;
       const int hn = h + a.mid_h[j];
       const double base = Sg - sc.NK;
-      // thresholds on the scaled tables
-      double thC = 0.0, thX = 0.0, thN = 0.0;
-      if (kAC_ || kAP_) thC = (-base / Sn) * sc.sc_up[0];
-      if (kFL_) thX = (Mxn / Sn) * sc.sc_up[1];
-      if (kFLP_) thN = (fmin(Mnn, sc.K) / Sn) * sc.sc_up[2];
+      const double rS = 1.0 / Sn;
+      const double thC = (kAC_ || kAP_) ? -base * rS : 0.0;
+      const double thX = kFL_ ? Mxn * rS : 0.0;
+      const double thN = kFLP_ ? fmin(Mnn, sc.K) * rS : 0.0;
 
-      // --- the leaf block: 2^L leaves, one compare + one masked FMA each
+      // --- the leaf block: 2^L explicit leaf tests per table
       double accC[NC], accP[NC], accX[NC], accN[NC];
-      unsigned cntC[NC], cntP[NC], cntX[NC], cntN[NC];
+      int cntC[NC], cntP[NC], cntX[NC], cntN[NC];
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
         accC[c] = accP[c] = accX[c] = accN[c] = 0.0;
-        cntC[c] = cntP[c] = cntX[c] = cntN[c] = 0u;
+        cntC[c] = cntP[c] = cntX[c] = cntN[c] = 0;
       }
-      const int off = j & sc.zero;  // 0, opaque to the compiler
-      constexpr int NT = (int)(kAC_ || kAP_) + (int)kFL_ + (int)kFLP_;  // tables in use (<= 2)
-      const double2* tb = reinterpret_cast<const double2*>(NT == 2 ? stab : a.tab) + off;
-#pragma unroll
-      for (int s2 = 0; s2 < NL / 2; ++s2) {
-        // NT == 1: one double2 = leaves (2 s2, 2 s2 + 1) of the single table
-        // NT == 2: two double2 = (first, second) table values of the two leaves
-        double2 va = make_double2(0.0, 0.0), vb = make_double2(0.0, 0.0);
-        if (NT == 1) va = tb[s2];
-        if (NT == 2) { va = tb[2 * s2]; vb = tb[2 * s2 + 1]; }
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          const int s = 2 * s2 + hh;
-          const int cls = __popc(s);
-          const double x0 = (NT == 1) ? (hh ? va.y : va.x) : (hh ? vb.x : va.x);
-          const double x1 = (NT == 1) ? 0.0 : (hh ? vb.y : va.y);
-          if (kAC_ || kAP_) {
-            const double c = x0;
-            if (kAC_) {
-              const unsigned mh = (c > thC) ? kMaskHi : 0u;
-              accC[cls] = fma(__hiloint2double((int)mh, zlo), c, accC[cls]);
-              cntC[cls] += mh;
-            }
-            if (kAP_) {
-              const unsigned mh = (c < thC) ? kMaskHi : 0u;
-              accP[cls] = fma(__hiloint2double((int)mh, zlo), c, accP[cls]);
-              cntP[cls] += mh;
-            }
-          }
-          if (kFL_) {
-            const double c = (kAC_ || kAP_) ? x1 : x0;
-            const unsigned mh = (c > thX) ? kMaskHi : 0u;
-            accX[cls] = fma(__hiloint2double((int)mh, zlo), c, accX[cls]);
-            cntX[cls] += mh;
-          }
-          if (kFLP_) {
-            const double c = (kAC_ || kAP_ || kFL_) ? x1 : x0;
-            const unsigned mh = (c < thN) ? kMaskHi : 0u;
-            accN[cls] = fma(__hiloint2double((int)mh, zlo), c, accN[cls]);
-            cntN[cls] += mh;
-          }
-        }
-      }
+      const double2* tb = reinterpret_cast<const double2*>(a.tab) + (j & sc.zero);  // + 0, opaque
+      if (kAC_) leaf_block<L, NT, slotAC, true>(tb, sgpre[slotAC], thC, accC, cntC);
+      if (kAP_) leaf_block<L, NT, slotAP, false>(tb, sgpre[slotAP], thC, accP, cntP);
+      if (kFL_) leaf_block<L, NT, slotFL, true>(tb, sgpre[slotFL], thX, accX, cntX);
+      if (kFLP_) leaf_block<L, NT, slotFLP, false>(tb, sgpre[slotFLP], thN, accN, cntN);
+
       // --- class finalisation: node value = sum_c w[h+c] * contrib_c
       double vAC = 0.0, vAP = 0.0, vFL = 0.0, vFLP = 0.0, vEC = 0.0, vEP = 0.0;
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
         const double wv = sw[hn + c];
         const double bc = a.b_cls[c];
-        if (kAC_) {
-          const double A = accC[c] * sc.sc_dn[0];
-          const double n = u32_to_double(cntC[c] >> 24);
-          vAC = fma(wv, fma(Sn, A, base * n), vAC);
-        }
-        if (kAP_) {
-          const double A = accP[c] * sc.sc_dn[0];
-          const double n = u32_to_double(cntP[c] >> 24);
-          vAP = fma(wv, fma(-Sn, A, -base * n), vAP);
-        }
+        if (kAC_) vAC = fma(wv, fma(Sn, accC[c], base * (double)cntC[c]), vAC);
+        if (kAP_) vAP = fma(wv, fma(-Sn, accP[c], -base * (double)cntP[c]), vAP);
         if (kFL_) {
-          const double A = accX[c] * sc.sc_dn[1];
-          const double n = u32_to_double(cntX[c] >> 24);
           // S A + Mx (C_c - n) - S e_c C_c
-          const double t = fma(Sn, A, Mxn * (bc - n));
+          const double t = fma(Sn, accX[c], Mxn * (bc - (double)cntX[c]));
           vFL = fma(wv, fma(-Sn * a.e_cls[c], bc, t), vFL);
         }
         if (kFLP_) {
-          const double A = accN[c] * sc.sc_dn[2];
-          const double n = u32_to_double(cntN[c] >> 24);
-          const double flat = fmax(sc.K - Mnn, 0.0);
-          const double t = fma(sc.K, n, -Sn * A);
-          vFLP = fma(wv, fma(bc - n, flat, t), vFLP);
+          const double n = (double)cntN[c];
+          const double t = fma(sc.K, n, -Sn * accN[c]);
+          vFLP = fma(wv, fma(bc - n, fmax(sc.K - Mnn, 0.0), t), vFLP);
         }
         if (kEC_) vEC = fma(wv, bc * fmax(fma(Sn, a.e_cls[c], -sc.K), 0.0), vEC);
         if (kEP_) vEP = fma(wv, bc * fmax(fma(-Sn, a.e_cls[c], sc.K), 0.0), vEP);
@@ -172,10 +164,10 @@ k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_
         // leaf bookkeeping (K6): leaves per total up count, code coverage
         const unsigned long long node = (tp << sc.m) | (unsigned long long)j;
 #pragma unroll
-        for (int c = 0; c < NC; ++c) atomicAdd(&shist[hn + c], (unsigned long long)a.b_cls[c]);
-        leaves += (unsigned long long)NL;
+        for (int c = 0; c < NC; ++c) atomicAdd(&shist[hn + c], (unsigned long long)binom(L, c));
+        leaves += 1ull << L;
         // sum of codes node*2^L + s, s < 2^L
-        code_sum += (node << (2 * L)) + (((unsigned long long)NL * (NL - 1)) >> 1);
+        code_sum += (node << (2 * L)) + (((1ull << L) * ((1ull << L) - 1)) >> 1);
       }
     }
    }  // rr
@@ -345,6 +337,7 @@ cudaError_t launch_exact_fast(int L, unsigned km, const void* args, bool cnt, in
 #define BP_CASE(LL, KMV) \
   if (L == LL && km == (KMV)) return launch_fast_t<LL, (KMV)>(args, cnt, grid, st, unit_out, hist);
   BP_FAST_KMS(BP_CASE, 8)
+  BP_FAST_KMS(BP_CASE, 9)
 #undef BP_CASE
   return cudaErrorInvalidValue;
 }
@@ -353,6 +346,7 @@ int occupancy_exact_fast(int L, unsigned km, bool cnt) {
 #define BP_CASE(LL, KMV) \
   if (L == LL && km == (KMV)) return occupancy_fast_t<LL, (KMV)>(cnt);
   BP_FAST_KMS(BP_CASE, 8)
+  BP_FAST_KMS(BP_CASE, 9)
 #undef BP_CASE
   return 0;
 }
@@ -360,6 +354,7 @@ int occupancy_exact_fast(int L, unsigned km, bool cnt) {
 size_t exact_args_size(int L) {
   switch (L) {
     case 8: return sizeof(ExactArgs<8>);
+    case 9: return sizeof(ExactArgs<9>);
     default: return 0;
   }
 }
