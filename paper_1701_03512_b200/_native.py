@@ -16,7 +16,7 @@ import numpy as np
 from . import errors as E
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libbinpaths_b200.so")
+LIB_PATH = os.environ.get("BINPATHS_LIB") or os.path.join(_HERE, "_lib", "libbinpaths_b200.so")
 N_PAYOFFS = 6
 
 FLAG_COUNT = 1

@@ -153,7 +153,7 @@ static Layout choose_layout(const bp_tree* t, uint32_t payoffs, uint32_t flags, 
     lay.L = fast_L();
     lay.D = N - lay.L;
     const int free_bits = lay.D - 5;  // bits above the lane
-    lay.m = std::max(0, std::min(6, free_bits - kUnitTargetLog2));
+    lay.m = std::max(1, std::min(6, free_bits - kUnitTargetLog2));  // >= 1: nodes go in pairs
     lay.Dp = lay.D - lay.m;
     const int unit_bits = free_bits - lay.m;
     lay.q = std::max(0, unit_bits - 18);
@@ -194,11 +194,11 @@ static void kind_table_layout(int kind, const std::vector<double>& c, const std:
     for (size_t i = 0; i < cls.size(); ++i) pos_out[start + i] = cls[i];
     for (int g = 0; g < class_groups(L, cl); ++g) {
       double* P = gpre[group_base(L, cl) + g];
-      const int len = std::min<int>(8, (int)cls.size() - 8 * g);
+      const int len = std::min<int>(kGroup, (int)cls.size() - kGroup * g);
       double sum = 0.0, comp = 0.0;  // compensated prefix sums, rounded once
       P[0] = 0.0;
       for (int n = 1; n < kGroupSlots; ++n) {
-        if (n <= len) comp_add(sum, comp, cls[8 * g + n - 1]);
+        if (n <= len) comp_add(sum, comp, cls[kGroup * g + n - 1]);
         P[n] = sum + comp;
       }
     }

@@ -24,7 +24,7 @@
 //   in-the-money leaf contributes S c_s + (Sig - N K).
 // * the inner table is laid out by up-count class c = |s| and, inside a
 //   class, sorted in the compare direction (host side, per tree), then cut
-//   into groups of <= 8 positions.  Inside a group the in-the-money leaves
+//   into groups of <= kGroup positions.  Inside a group the in-the-money leaves
 //   are therefore a prefix: the per-leaf compares (DSETP + predicated
 //   increment) give the count n, and the group's contribution sum_ITM c_s
 //   is the precomputed prefix sum P_g[n] (one shared-memory load per group).
@@ -76,14 +76,18 @@ __host__ __device__ constexpr int class_start(int L, int c) {
   for (int i = 0; i < c; ++i) s += binom(L, i);
   return s;
 }
-__host__ __device__ constexpr int class_groups(int L, int c) { return (binom(L, c) + 7) / 8; }
+#ifndef BP_GROUP
+#define BP_GROUP 8
+#endif
+constexpr int kGroup = BP_GROUP;  // leaves per sorted group (prefix-sum lookup granularity)
+__host__ __device__ constexpr int class_groups(int L, int c) { return (binom(L, c) + kGroup - 1) / kGroup; }
 __host__ __device__ constexpr int group_base(int L, int c) {
   int s = 0;
   for (int i = 0; i < c; ++i) s += class_groups(L, i);
   return s;
 }
 __host__ __device__ constexpr int n_groups(int L) { return group_base(L, L + 1); }
-constexpr int kGroupSlots = 9;  // prefix sums for n = 0..8
+constexpr int kGroupSlots = kGroup + 1;  // prefix sums for n = 0..kGroup
 
 template <int L>
 struct __align__(16) ExactArgs {

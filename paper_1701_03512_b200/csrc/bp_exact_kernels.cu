@@ -5,6 +5,10 @@
 #include "bp_exact.cuh"
 #include "bp_kernels.h"
 
+#ifndef BP_TAB_SMEM
+#define BP_TAB_SMEM 0  // inner tables: 0 = constant bank (uniform LDCU), 1 = shared memory (LDS.128)
+#endif
+
 namespace bp {
 
 // ---------------------------------------------------------------------------
@@ -17,42 +21,49 @@ __device__ __forceinline__ void leaf_test(int& n, double x, double th) {
     asm("{.reg .pred p; setp.lt.f64 p, %1, %2; @p add.s32 %0, %0, 1;}" : "+r"(n) : "d"(x), "d"(th));
 }
 
-// The leaf block of one table slot: every position i of the 2^L inner
-// leaves is tested once; per group of <= 8 the ITM count n selects the
-// group's prefix sum.  acc[c] / cnt[c]: per-class ITM sum and count.
-// Compile-time recursion over (class C, group G) so every index is constant.
-template <int L, int NT, int SLOT, bool GT, int C, int G>
+// The leaf block of one table slot for NP nodes at once: every position i of
+// the 2^L inner leaves is loaded once (uniform LDCU) and tested against each
+// node's threshold; per group of <= kGroup the ITM count n selects the
+// group's prefix sum.  acc[p][c] / cnt[p][c]: per-node, per-class ITM sum and
+// count.  Compile-time recursion over (class C, group G): every index is constant.
+template <int L, int NP, int SLOT, bool GT, int C, int G>
 struct LeafGroups {
-  static __device__ __forceinline__ void run(const double2* __restrict__ tb, const double* __restrict__ gpre, double th,
-                                             double (&acc)[L + 1], int (&cnt)[L + 1]) {
+  static __device__ __forceinline__ void run(const double2* __restrict__ tb, const double* __restrict__ gpre,
+                                             const double (&th)[NP], double (&acc)[NP][L + 1], int (&cnt)[NP][L + 1]) {
     if constexpr (C <= L) {
       constexpr int size = binom(L, C);
-      if constexpr (8 * G < size) {
-        constexpr int len = (size - 8 * G) < 8 ? (size - 8 * G) : 8;
-        constexpr int i0 = class_start(L, C) + 8 * G;
-        int n = 0;
+      if constexpr (kGroup * G < size) {
+        constexpr int len = (size - kGroup * G) < kGroup ? (size - kGroup * G) : kGroup;
+        constexpr int i0 = class_start(L, C) + kGroup * G;
+        int n[NP];
+#pragma unroll
+        for (int p = 0; p < NP; ++p) n[p] = 0;
 #pragma unroll
         for (int j = 0; j < len; ++j) {
           // 16-byte loads of positions (2k, 2k+1) of this slot's table
           const int i = SLOT * (1 << L) + i0 + j;
           const double2 v = tb[i >> 1];
           const double x = (i & 1) ? v.y : v.x;
-          leaf_test<GT>(n, x, th);
+#pragma unroll
+          for (int p = 0; p < NP; ++p) leaf_test<GT>(n[p], x, th[p]);
         }
-        acc[C] += gpre[(group_base(L, C) + G) * kGroupSlots + n];
-        cnt[C] += n;
-        LeafGroups<L, NT, SLOT, GT, C, G + 1>::run(tb, gpre, th, acc, cnt);
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          acc[p][C] += gpre[(group_base(L, C) + G) * kGroupSlots + n[p]];
+          cnt[p][C] += n[p];
+        }
+        LeafGroups<L, NP, SLOT, GT, C, G + 1>::run(tb, gpre, th, acc, cnt);
       } else {
-        LeafGroups<L, NT, SLOT, GT, C + 1, 0>::run(tb, gpre, th, acc, cnt);
+        LeafGroups<L, NP, SLOT, GT, C + 1, 0>::run(tb, gpre, th, acc, cnt);
       }
     }
   }
 };
 
-template <int L, int NT, int SLOT, bool GT>
-__device__ __forceinline__ void leaf_block(const double2* __restrict__ tb, const double* __restrict__ gpre, double th,
-                                           double (&acc)[L + 1], int (&cnt)[L + 1]) {
-  LeafGroups<L, NT, SLOT, GT, 0, 0>::run(tb, gpre, th, acc, cnt);
+template <int L, int NP, int SLOT, bool GT>
+__device__ __forceinline__ void leaf_block(const double2* __restrict__ tb, const double* __restrict__ gpre,
+                                           const double (&th)[NP], double (&acc)[NP][L + 1], int (&cnt)[NP][L + 1]) {
+  LeafGroups<L, NP, SLOT, GT, 0, 0>::run(tb, gpre, th, acc, cnt);
 }
 
 // K1: affine-threshold enumeration.  KM = compile-time kind mask.
@@ -69,10 +80,17 @@ k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_
   constexpr int NT = (int)kAC_ + (int)kAP_ + (int)kFL_ + (int)kFLP_;
   static_assert(NT <= 2, "at most two tables per launch");
   constexpr int slotAC = 0, slotAP = (int)kAC_, slotFL = (int)kAC_ + (int)kAP_, slotFLP = slotFL + (int)kFL_;
+  // nodes per leaf block: each table load feeds NP compares.  Two-table
+  // (fused) kernels stay at NP = 1 to keep registers <= 64 (occupancy).
+  constexpr int NP = (NT == 2) ? 1 : 2;
 
   __shared__ double sw[kMaxN + 2 + NC];
   __shared__ unsigned long long shist[kMaxN + 2];
   __shared__ double sgpre[NT > 0 ? NT : 1][NG * kGroupSlots];
+#if BP_TAB_SMEM
+  __shared__ __align__(16) double stab[NT > 0 ? NT << L : 2];
+  for (int i = threadIdx.x; i < (NT << L); i += blockDim.x) stab[i] = a.tab[i];
+#endif
   for (int i = threadIdx.x; i < kMaxN + 2 + NC; i += blockDim.x) sw[i] = (i < kMaxN + 2) ? a.w[i] : 0.0;
   for (int t = 0; t < NT; ++t)
     for (int i = threadIdx.x; i < NG * kGroupSlots; i += blockDim.x) sgpre[t][i] = (&a.gpre[t][0][0])[i];
@@ -105,69 +123,85 @@ k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_
       h += b;
     }
 
-    for (int j = 0; j < sc.n_mid; ++j) {
-      // --- node state at depth D
-      const double Sn = S * a.mid_e[j];
-      const double Sg = fma(S, a.mid_c[j], Sig);
-      const double Mxn = needMx ? fmax(Mx, S * a.mid_mx[j]) : 0.0;
-      const double Mnn = needMn ? fmin(Mn, S * a.mid_mn[j]) : 0.0;
-      const int hn = h + a.mid_h[j];
-      const double base = Sg - sc.NK;
-      const double rS = 1.0 / Sn;
-      const double thC = (kAC_ || kAP_) ? -base * rS : 0.0;
-      const double thX = kFL_ ? Mxn * rS : 0.0;
-      const double thN = kFLP_ ? fmin(Mnn, sc.K) * rS : 0.0;
-
-      // --- the leaf block: 2^L explicit leaf tests per table
-      double accC[NC], accP[NC], accX[NC], accN[NC];
-      int cntC[NC], cntP[NC], cntX[NC], cntN[NC];
+    // nodes are processed NP at a time (n_mid is a multiple of NP: m >= 1)
+    for (int j0 = 0; j0 < sc.n_mid; j0 += NP) {
+      double Sn[NP], Sg[NP], Mxn[NP], Mnn[NP], base[NP], thC[NP], thX[NP], thN[NP];
+      int hn[NP];
 #pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        accC[c] = accP[c] = accX[c] = accN[c] = 0.0;
-        cntC[c] = cntP[c] = cntX[c] = cntN[c] = 0;
+      for (int p = 0; p < NP; ++p) {
+        // --- node state at depth D
+        const int j = j0 + p;
+        Sn[p] = S * a.mid_e[j];
+        Sg[p] = fma(S, a.mid_c[j], Sig);
+        Mxn[p] = needMx ? fmax(Mx, S * a.mid_mx[j]) : 0.0;
+        Mnn[p] = needMn ? fmin(Mn, S * a.mid_mn[j]) : 0.0;
+        hn[p] = h + a.mid_h[j];
+        base[p] = Sg[p] - sc.NK;
+        const double rS = 1.0 / Sn[p];
+        thC[p] = (kAC_ || kAP_) ? -base[p] * rS : 0.0;
+        thX[p] = kFL_ ? Mxn[p] * rS : 0.0;
+        thN[p] = kFLP_ ? fmin(Mnn[p], sc.K) * rS : 0.0;
       }
-      const double2* tb = reinterpret_cast<const double2*>(a.tab) + (j & sc.zero);  // + 0, opaque
-      if (kAC_) leaf_block<L, NT, slotAC, true>(tb, sgpre[slotAC], thC, accC, cntC);
-      if (kAP_) leaf_block<L, NT, slotAP, false>(tb, sgpre[slotAP], thC, accP, cntP);
-      if (kFL_) leaf_block<L, NT, slotFL, true>(tb, sgpre[slotFL], thX, accX, cntX);
-      if (kFLP_) leaf_block<L, NT, slotFLP, false>(tb, sgpre[slotFLP], thN, accN, cntN);
 
-      // --- class finalisation: node value = sum_c w[h+c] * contrib_c
-      double vAC = 0.0, vAP = 0.0, vFL = 0.0, vFLP = 0.0, vEC = 0.0, vEP = 0.0;
+      // --- the leaf block: 2^L explicit leaf tests per table per node
+      double accC[NP][NC], accP[NP][NC], accX[NP][NC], accN[NP][NC];
+      int cntC[NP][NC], cntP[NP][NC], cntX[NP][NC], cntN[NP][NC];
 #pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        const double wv = sw[hn + c];
-        const double bc = a.b_cls[c];
-        if (kAC_) vAC = fma(wv, fma(Sn, accC[c], base * (double)cntC[c]), vAC);
-        if (kAP_) vAP = fma(wv, fma(-Sn, accP[c], -base * (double)cntP[c]), vAP);
-        if (kFL_) {
-          // S A + Mx (C_c - n) - S e_c C_c
-          const double t = fma(Sn, accX[c], Mxn * (bc - (double)cntX[c]));
-          vFL = fma(wv, fma(-Sn * a.e_cls[c], bc, t), vFL);
+      for (int p = 0; p < NP; ++p)
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          accC[p][c] = accP[p][c] = accX[p][c] = accN[p][c] = 0.0;
+          cntC[p][c] = cntP[p][c] = cntX[p][c] = cntN[p][c] = 0;
         }
-        if (kFLP_) {
-          const double n = (double)cntN[c];
-          const double t = fma(sc.K, n, -Sn * accN[c]);
-          vFLP = fma(wv, fma(bc - n, fmax(sc.K - Mnn, 0.0), t), vFLP);
-        }
-        if (kEC_) vEC = fma(wv, bc * fmax(fma(Sn, a.e_cls[c], -sc.K), 0.0), vEC);
-        if (kEP_) vEP = fma(wv, bc * fmax(fma(-Sn, a.e_cls[c], sc.K), 0.0), vEP);
-      }
-      if (kAC_) comp_add(ts[kAC], tc[kAC], vAC);
-      if (kAP_) comp_add(ts[kAP], tc[kAP], vAP);
-      if (kFL_) comp_add(ts[kFL], tc[kFL], vFL);
-      if (kFLP_) comp_add(ts[kFLP], tc[kFLP], vFLP);
-      if (kEC_) comp_add(ts[kEC], tc[kEC], vEC);
-      if (kEP_) comp_add(ts[kEP], tc[kEP], vEP);
+#if BP_TAB_SMEM
+      const double2* tb = reinterpret_cast<const double2*>(stab) + (j0 & sc.zero);  // + 0, opaque
+#else
+      const double2* tb = reinterpret_cast<const double2*>(a.tab) + (j0 & sc.zero);  // + 0, opaque
+#endif
+      if (kAC_) leaf_block<L, NP, slotAC, true>(tb, sgpre[slotAC], thC, accC, cntC);
+      if (kAP_) leaf_block<L, NP, slotAP, false>(tb, sgpre[slotAP], thC, accP, cntP);
+      if (kFL_) leaf_block<L, NP, slotFL, true>(tb, sgpre[slotFL], thX, accX, cntX);
+      if (kFLP_) leaf_block<L, NP, slotFLP, false>(tb, sgpre[slotFLP], thN, accN, cntN);
 
-      if (CNT) {
-        // leaf bookkeeping (K6): leaves per total up count, code coverage
-        const unsigned long long node = (tp << sc.m) | (unsigned long long)j;
 #pragma unroll
-        for (int c = 0; c < NC; ++c) atomicAdd(&shist[hn + c], (unsigned long long)binom(L, c));
-        leaves += 1ull << L;
-        // sum of codes node*2^L + s, s < 2^L
-        code_sum += (node << (2 * L)) + (((1ull << L) * ((1ull << L) - 1)) >> 1);
+      for (int p = 0; p < NP; ++p) {
+        // --- class finalisation: node value = sum_c w[h+c] * contrib_c
+        double vAC = 0.0, vAP = 0.0, vFL = 0.0, vFLP = 0.0, vEC = 0.0, vEP = 0.0;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          const double wv = sw[hn[p] + c];
+          const double bc = a.b_cls[c];
+          if (kAC_) vAC = fma(wv, fma(Sn[p], accC[p][c], base[p] * (double)cntC[p][c]), vAC);
+          if (kAP_) vAP = fma(wv, fma(-Sn[p], accP[p][c], -base[p] * (double)cntP[p][c]), vAP);
+          if (kFL_) {
+            // S A + Mx (C_c - n) - S e_c C_c
+            const double t = fma(Sn[p], accX[p][c], Mxn[p] * (bc - (double)cntX[p][c]));
+            vFL = fma(wv, fma(-Sn[p] * a.e_cls[c], bc, t), vFL);
+          }
+          if (kFLP_) {
+            const double n = (double)cntN[p][c];
+            const double t = fma(sc.K, n, -Sn[p] * accN[p][c]);
+            vFLP = fma(wv, fma(bc - n, fmax(sc.K - Mnn[p], 0.0), t), vFLP);
+          }
+          if (kEC_) vEC = fma(wv, bc * fmax(fma(Sn[p], a.e_cls[c], -sc.K), 0.0), vEC);
+          if (kEP_) vEP = fma(wv, bc * fmax(fma(-Sn[p], a.e_cls[c], sc.K), 0.0), vEP);
+        }
+        if (kAC_) comp_add(ts[kAC], tc[kAC], vAC);
+        if (kAP_) comp_add(ts[kAP], tc[kAP], vAP);
+        if (kFL_) comp_add(ts[kFL], tc[kFL], vFL);
+        if (kFLP_) comp_add(ts[kFLP], tc[kFLP], vFLP);
+        if (kEC_) comp_add(ts[kEC], tc[kEC], vEC);
+        if (kEP_) comp_add(ts[kEP], tc[kEP], vEP);
+
+        if (CNT) {
+          // leaf bookkeeping (K6): leaves per total up count, code coverage
+          const unsigned long long node = (tp << sc.m) | (unsigned long long)(j0 + p);
+#pragma unroll
+          for (int c = 0; c < NC; ++c) atomicAdd(&shist[hn[p] + c], (unsigned long long)binom(L, c));
+          leaves += 1ull << L;
+          // sum of codes node*2^L + s, s < 2^L
+          code_sum += (node << (2 * L)) + (((1ull << L) * ((1ull << L) - 1)) >> 1);
+        }
       }
     }
    }  // rr
