@@ -60,6 +60,17 @@ struct LeafGroups {
   }
 };
 
+template <int NP, int NC>
+__device__ __forceinline__ void zero_acc(double (&acc)[NP][NC], int (&cnt)[NP][NC]) {
+#pragma unroll
+  for (int p = 0; p < NP; ++p)
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      acc[p][c] = 0.0;
+      cnt[p][c] = 0;
+    }
+}
+
 template <int L, int NP, int SLOT, bool GT>
 __device__ __forceinline__ void leaf_block(const double2* __restrict__ tb, const double* __restrict__ gpre,
                                            const double (&th)[NP], double (&acc)[NP][L + 1], int (&cnt)[NP][L + 1]) {
@@ -67,8 +78,13 @@ __device__ __forceinline__ void leaf_block(const double2* __restrict__ tb, const
 }
 
 // K1: affine-threshold enumeration.  KM = compile-time kind mask.
+// resident CTAs per SM the register allocation targets: 3 for one table
+// (<= 85 registers), 2 for the fused two-table kernels (measured best, r1)
+__host__ __device__ constexpr int fast_tables(unsigned km) {
+  return (int)((km >> kAC) & 1) + (int)((km >> kAP) & 1) + (int)((km >> kFL) & 1) + (int)((km >> kFLP) & 1);
+}
 template <int L, unsigned KM, bool CNT>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, fast_tables(KM) == 2 ? 2 : 3)
 k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_out,
              unsigned long long* __restrict__ hist) {
   constexpr int NC = L + 1;
@@ -80,9 +96,8 @@ k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_
   constexpr int NT = (int)kAC_ + (int)kAP_ + (int)kFL_ + (int)kFLP_;
   static_assert(NT <= 2, "at most two tables per launch");
   constexpr int slotAC = 0, slotAP = (int)kAC_, slotFL = (int)kAC_ + (int)kAP_, slotFLP = slotFL + (int)kFL_;
-  // nodes per leaf block: each table load feeds NP compares.  Two-table
-  // (fused) kernels stay at NP = 1 to keep registers <= 64 (occupancy).
-  constexpr int NP = (NT == 2) ? 1 : 2;
+  // nodes per leaf block: each table load feeds NP compares
+  constexpr int NP = 2;
 
   __shared__ double sw[kMaxN + 2 + NC];
   __shared__ unsigned long long shist[kMaxN + 2];
@@ -143,57 +158,94 @@ k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_
         thN[p] = kFLP_ ? fmin(Mnn[p], sc.K) * rS : 0.0;
       }
 
-      // --- the leaf block: 2^L explicit leaf tests per table per node
-      double accC[NP][NC], accP[NP][NC], accX[NP][NC], accN[NP][NC];
-      int cntC[NP][NC], cntP[NP][NC], cntX[NP][NC], cntN[NP][NC];
-#pragma unroll
-      for (int p = 0; p < NP; ++p)
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-          accC[p][c] = accP[p][c] = accX[p][c] = accN[p][c] = 0.0;
-          cntC[p][c] = cntP[p][c] = cntX[p][c] = cntN[p][c] = 0;
-        }
 #if BP_TAB_SMEM
       const double2* tb = reinterpret_cast<const double2*>(stab) + (j0 & sc.zero);  // + 0, opaque
 #else
       const double2* tb = reinterpret_cast<const double2*>(a.tab) + (j0 & sc.zero);  // + 0, opaque
 #endif
-      if (kAC_) leaf_block<L, NP, slotAC, true>(tb, sgpre[slotAC], thC, accC, cntC);
-      if (kAP_) leaf_block<L, NP, slotAP, false>(tb, sgpre[slotAP], thC, accP, cntP);
-      if (kFL_) leaf_block<L, NP, slotFL, true>(tb, sgpre[slotFL], thX, accX, cntX);
-      if (kFLP_) leaf_block<L, NP, slotFLP, false>(tb, sgpre[slotFLP], thN, accN, cntN);
-
+      // --- per kind: the leaf block (2^L explicit leaf tests per node), then
+      // the class finalisation, node value = sum_c w[h+c] * contrib_c.  Kinds
+      // run one after the other so only one kind's accumulators are live.
+      if (kAC_) {
+        double acc[NP][NC];
+        int cnt[NP][NC];
+        zero_acc<NP, NC>(acc, cnt);
+        leaf_block<L, NP, slotAC, true>(tb, sgpre[slotAC], thC, acc, cnt);
 #pragma unroll
-      for (int p = 0; p < NP; ++p) {
-        // --- class finalisation: node value = sum_c w[h+c] * contrib_c
-        double vAC = 0.0, vAP = 0.0, vFL = 0.0, vFLP = 0.0, vEC = 0.0, vEP = 0.0;
+        for (int p = 0; p < NP; ++p) {
+          double v = 0.0;
 #pragma unroll
-        for (int c = 0; c < NC; ++c) {
-          const double wv = sw[hn[p] + c];
-          const double bc = a.b_cls[c];
-          if (kAC_) vAC = fma(wv, fma(Sn[p], accC[p][c], base[p] * (double)cntC[p][c]), vAC);
-          if (kAP_) vAP = fma(wv, fma(-Sn[p], accP[p][c], -base[p] * (double)cntP[p][c]), vAP);
-          if (kFL_) {
-            // S A + Mx (C_c - n) - S e_c C_c
-            const double t = fma(Sn[p], accX[p][c], Mxn[p] * (bc - (double)cntX[p][c]));
-            vFL = fma(wv, fma(-Sn[p] * a.e_cls[c], bc, t), vFL);
-          }
-          if (kFLP_) {
-            const double n = (double)cntN[p][c];
-            const double t = fma(sc.K, n, -Sn[p] * accN[p][c]);
-            vFLP = fma(wv, fma(bc - n, fmax(sc.K - Mnn[p], 0.0), t), vFLP);
-          }
-          if (kEC_) vEC = fma(wv, bc * fmax(fma(Sn[p], a.e_cls[c], -sc.K), 0.0), vEC);
-          if (kEP_) vEP = fma(wv, bc * fmax(fma(-Sn[p], a.e_cls[c], sc.K), 0.0), vEP);
+          for (int c = 0; c < NC; ++c) v = fma(sw[hn[p] + c], fma(Sn[p], acc[p][c], base[p] * (double)cnt[p][c]), v);
+          comp_add(ts[kAC], tc[kAC], v);
         }
-        if (kAC_) comp_add(ts[kAC], tc[kAC], vAC);
-        if (kAP_) comp_add(ts[kAP], tc[kAP], vAP);
-        if (kFL_) comp_add(ts[kFL], tc[kFL], vFL);
-        if (kFLP_) comp_add(ts[kFLP], tc[kFLP], vFLP);
-        if (kEC_) comp_add(ts[kEC], tc[kEC], vEC);
-        if (kEP_) comp_add(ts[kEP], tc[kEP], vEP);
+      }
+      if (kAP_) {
+        double acc[NP][NC];
+        int cnt[NP][NC];
+        zero_acc<NP, NC>(acc, cnt);
+        leaf_block<L, NP, slotAP, false>(tb, sgpre[slotAP], thC, acc, cnt);
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          double v = 0.0;
+#pragma unroll
+          for (int c = 0; c < NC; ++c) v = fma(sw[hn[p] + c], fma(-Sn[p], acc[p][c], -base[p] * (double)cnt[p][c]), v);
+          comp_add(ts[kAP], tc[kAP], v);
+        }
+      }
+      if (kFL_) {
+        double acc[NP][NC];
+        int cnt[NP][NC];
+        zero_acc<NP, NC>(acc, cnt);
+        leaf_block<L, NP, slotFL, true>(tb, sgpre[slotFL], thX, acc, cnt);
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          double v = 0.0;
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            // S A + Mx (C_c - n) - S e_c C_c
+            const double bc = a.b_cls[c];
+            const double t = fma(Sn[p], acc[p][c], Mxn[p] * (bc - (double)cnt[p][c]));
+            v = fma(sw[hn[p] + c], fma(-Sn[p] * a.e_cls[c], bc, t), v);
+          }
+          comp_add(ts[kFL], tc[kFL], v);
+        }
+      }
+      if (kFLP_) {
+        double acc[NP][NC];
+        int cnt[NP][NC];
+        zero_acc<NP, NC>(acc, cnt);
+        leaf_block<L, NP, slotFLP, false>(tb, sgpre[slotFLP], thN, acc, cnt);
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          double v = 0.0;
+          const double flat = fmax(sc.K - Mnn[p], 0.0);
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            const double n = (double)cnt[p][c];
+            const double t = fma(sc.K, n, -Sn[p] * acc[p][c]);
+            v = fma(sw[hn[p] + c], fma(a.b_cls[c] - n, flat, t), v);
+          }
+          comp_add(ts[kFLP], tc[kFLP], v);
+        }
+      }
+      if (kEC_ || kEP_) {
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          double vEC = 0.0, vEP = 0.0;
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            const double wv = sw[hn[p] + c], bc = a.b_cls[c];
+            if (kEC_) vEC = fma(wv, bc * fmax(fma(Sn[p], a.e_cls[c], -sc.K), 0.0), vEC);
+            if (kEP_) vEP = fma(wv, bc * fmax(fma(-Sn[p], a.e_cls[c], sc.K), 0.0), vEP);
+          }
+          if (kEC_) comp_add(ts[kEC], tc[kEC], vEC);
+          if (kEP_) comp_add(ts[kEP], tc[kEP], vEP);
+        }
+      }
 
-        if (CNT) {
+      if (CNT) {
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
           // leaf bookkeeping (K6): leaves per total up count, code coverage
           const unsigned long long node = (tp << sc.m) | (unsigned long long)(j0 + p);
 #pragma unroll
