@@ -153,7 +153,11 @@ static Layout choose_layout(const bp_tree* t, uint32_t payoffs, uint32_t flags, 
     lay.L = fast_L();
     lay.D = N - lay.L;
     const int free_bits = lay.D - 5;  // bits above the lane
-    lay.m = std::max(1, std::min(6, free_bits - kUnitTargetLog2));  // >= 1: nodes go in pairs
+    static const int target = [] {
+      const char* e = std::getenv("BINPATHS_UNIT_LOG2");
+      return e ? std::atoi(e) : kUnitTargetLog2;
+    }();
+    lay.m = std::max(1, std::min(6, free_bits - target));  // >= 1: nodes go in pairs
     lay.Dp = lay.D - lay.m;
     const int unit_bits = free_bits - lay.m;
     lay.q = std::max(0, unit_bits - 18);

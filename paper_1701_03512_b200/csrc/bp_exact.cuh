@@ -47,7 +47,7 @@ BP_HD constexpr int kind_table(int k) {
 }
 
 constexpr int kMidMax = 64;          // 2^m, m <= 6
-constexpr int kUnitTargetLog2 = 15;  // units >= 2^15 when the tree allows it
+constexpr int kUnitTargetLog2 = 14;  // units >= 2^14 when the tree allows it (r1 scan)
 constexpr int kMaxSB = 8;            // canonical super-blocks (top 3 bits)
 constexpr int kFastMinN = 16;        // smaller trees use the per-path walk
 constexpr unsigned kMaskHi = 0x01000000u;  // mask double 2^(16-1023)
