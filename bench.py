@@ -225,6 +225,51 @@ def kernel_share(w, classic_crr, dev, reps=5):
     return min(ts)
 
 
+def secondary_configs(dev):
+    """BASELINE configs[3] (stratified MC, N=64, k=12, R_m=65536, vs basic MC
+    with the same total draws) and configs[4] (4096 Asian calls at N=24)."""
+    from types import SimpleNamespace
+    import numpy as np
+    import paper_1701_03512_b200 as bp
+    from paper_1701_03512_b200 import mc as bmc
+    out = {}
+    N, k, R_m = 64, 12, 65536
+    P = bp.classic_crr(N, 0.2, 0.05, 1.0)
+    req = object.__new__(bp.ValuationRequest)
+    for f, v in dict(inputs=SimpleNamespace(S0=100.0, K=100.0, q=0.05, sigma=0.2, T=1.0, N=N), params=P,
+                     kind=bp.ASIAN_CALL, workers=1, force_large=True, devices=[dev]).items():
+        object.__setattr__(req, f, v)
+    ms = []
+    for i in range(4):
+        _, _, t = bmc._strata_stats(req, k, [R_m] * (1 << k), 0, 0, 1)
+        ms.append(t)
+    t = min(ms[1:])
+    e = bp.estimate_partitioned_equal(req, bp.McConfig(R=R_m, M=1 << k, seed=0))
+    b = bp.estimate_basic(req, bp.McConfig(R=R_m << k, seed=0))
+    out["config4"] = {"workload": "stratified MC N=64, k=12 (4096 strata), R_m=65536, Asian call, Philox4x32-10",
+                      "value": (R_m << k) / (t * 1e-3), "unit": "draws/s", "kernel_ms": t,
+                      "estimate": e.value, "std_error": e.std_error, "basic_estimate": b.value,
+                      "basic_std_error": b.std_error, "variance_ratio_basic_over_equal": b.variance / e.variance,
+                      "reference_ratio_N62": 1.60}
+    n, Nb = 4096, 24
+    rng = np.random.default_rng(0)
+    S0 = rng.uniform(50, 150, n); m = rng.uniform(0.8, 1.2, n); K = m * S0
+    sigma = rng.uniform(0.1, 0.5, n); r = rng.uniform(0.0, 0.08, n); T = rng.uniform(0.25, 3.0, n)
+    u = np.array([math.exp(a * math.sqrt(b / Nb)) for a, b in zip(sigma, T)])
+    d = 1.0 / u
+    p = np.array([(math.exp(a * b / Nb) - dd) / (uu - dd) for a, b, uu, dd in zip(r, T, u, d)])
+    disc = np.array([math.exp(-a * b) for a, b in zip(r, T)])
+    ms = []
+    for i in range(3):
+        vals, t = bp.price_batch(Nb, S0, K, u, d, p, disc, bp.ASIAN_CALL, device=dev, with_time=True)
+        ms.append(t)
+    t = min(ms[1:])
+    out["config5"] = {"workload": "4096 Asian calls, N=24, parameters from default_rng(0)",
+                      "value": n * (1 << Nb) / (t * 1e-3), "unit": "paths/s", "kernel_ms": t,
+                      "value_option0": float(vals[0])}
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -272,6 +317,11 @@ def run_ours(args):
         extra = {"value": (1 << 36) / (ms3 * 1e-3), "unit": "paths/s", "ms_per_step": ms3,
                  "asian_call": v3["asian-call"]}
 
+    # configs[3] (stratified MC, N = 64) and configs[4] (batched exact) on rank 0's GPU
+    extra45 = {}
+    if rank == 0 and not args.no_config3:
+        extra45 = secondary_configs(dev)
+
     if rank != 0:
         if world > 1:
             dist.barrier()
@@ -317,7 +367,7 @@ def run_ours(args):
                    "r": w["r"], "sigma": w["sigma"], "T": w["T"], "parallelism": f"superblock-shard x{world}",
                    "l2": "flushed (256 MiB write) between timed steps", "engine": "affine-threshold" if sh.engine else
                    "path-walk", "inner_bits": sh.inner_bits, "superblocks": sh.n_sb},
-        "values": vals, "config3": extra or None, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+        "values": vals, "config3": extra or None, **extra45, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk.summary(),
     }
