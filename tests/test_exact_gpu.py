@@ -157,3 +157,28 @@ def test_guard_and_extreme_lattices():
     assert a.engine == "affine-threshold"
     for k in ALL:
         assert _close(a.values[k], b.values[k]), (k, a.values[k], b.values[k])
+
+
+def test_paper_values_N32_beta_crr():
+    """PAPER.md:389,534 exact values (82.115 / 93.196), reproduced by the
+    reference's own enumeration (tests/golden/exact_paper.json) -- matched to 1e-12."""
+    g = load_golden("exact_paper.json")
+    inputs = bp.MarketInputs(S0=g["S0"], K=g["K"], q=g["q"], sigma=g["sigma"], T=g["T"], N=32)
+    params = bp.derive_crr(inputs)
+    assert params.u == g["u"] and params.up_probs[0] == g["p"]
+    req = bp.ValuationRequest(inputs=inputs, params=params, kind=bp.PayoffKind.ASIAN_PUT, force_large=True)
+    res = bp.value_exact(req, kinds=[bp.PayoffKind.ASIAN_PUT, bp.PayoffKind.FIXED_LOOKBACK_PUT])
+    for tag in ("asian-put", "lookback-put"):
+        assert _close(res.values[tag], g["values"][tag]), (tag, res.values[tag], g["values"][tag])
+        assert round(res.values[tag], 3) == g["published"][tag]
+
+
+def test_config3_golden_N36_when_available():
+    import os
+    from conftest import GOLDEN
+    if not os.path.exists(os.path.join(GOLDEN, "exact_config3.json")):
+        pytest.skip("config 3 golden not generated yet (tools/make_goldens.py config3, ~90 min)")
+    g = load_golden("exact_config3.json")
+    req = _req(36, 100.0, 105.0, 0.03, 2.0, g["u"], g["d"], g["p"])
+    res = bp.value_exact(req, kinds=[bp.ASIAN_CALL])
+    assert _close(res.values["asian-call"], g["asian_call"]), (res.values, g["asian_call"])
