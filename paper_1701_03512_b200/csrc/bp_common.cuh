@@ -68,15 +68,11 @@ constexpr uint32_t kPhiloxW1 = 0xBB67AE85u;
 
 BP_HD void philox_round(uint32_t& c0, uint32_t& c1, uint32_t& c2, uint32_t& c3,
                         uint32_t k0, uint32_t k1) {
-#ifdef __CUDA_ARCH__
-  const uint32_t hi0 = __umulhi(kPhiloxM0, c0);
-  const uint32_t hi1 = __umulhi(kPhiloxM1, c2);
-#else
-  const uint32_t hi0 = (uint32_t)(((uint64_t)kPhiloxM0 * c0) >> 32);
-  const uint32_t hi1 = (uint32_t)(((uint64_t)kPhiloxM1 * c2) >> 32);
-#endif
-  const uint32_t lo0 = kPhiloxM0 * c0;
-  const uint32_t lo1 = kPhiloxM1 * c2;
+  // one 32x32 -> 64 multiply per lane (IMAD.WIDE.U32 on the device)
+  const uint64_t p0 = (uint64_t)kPhiloxM0 * c0;
+  const uint64_t p1 = (uint64_t)kPhiloxM1 * c2;
+  const uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+  const uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
   const uint32_t n0 = hi1 ^ c1 ^ k0;
   const uint32_t n2 = hi0 ^ c3 ^ k1;
   c0 = n0;

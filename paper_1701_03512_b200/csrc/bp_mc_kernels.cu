@@ -94,23 +94,66 @@ __device__ __forceinline__ double payoff_of(unsigned kind, const PathState& st, 
 }
 
 // Walk the N - r suffix steps of draw i on stream (m, rep) from state st.
-template <unsigned KIND>
-__device__ __forceinline__ PathState walk_suffix(const McArgs& a, PathState st, uint32_t i, uint32_t stream,
-                                                 uint32_t rep) {
+// CONSTP: every suffix step has the same threshold thr0 (the BASELINE trees);
+// `up` is then one ISETP against a register (OR'ed with the uniform p == 1
+// flag) instead of a per-step table load.
+// Nibble tables: 4 consecutive steps with up-pattern b (step 1 = bit 3):
+// relative price after the 4 steps (e), sum of the 4 relative prices (c),
+// their max (x) and min (n).  Built once per CTA in shared memory.
+struct Nib {
+  double e, c, x, n;
+};
+
+__device__ __forceinline__ void build_nib(const McArgs& a, Nib* nib) {
+  for (int b = threadIdx.x; b < 16; b += blockDim.x) {
+    double r = 1.0, c = 0.0, x = -INFINITY, n = INFINITY;
+    for (int l = 0; l < 4; ++l) {
+      r *= ((b >> (3 - l)) & 1) ? a.u : a.d;
+      c += r;
+      x = fmax(x, r);
+      n = fmin(n, r);
+    }
+    nib[b] = Nib{r, c, x, n};
+  }
+}
+
+// Walk the N - r suffix steps of draw i on stream (m, rep) from state st.
+// Full blocks of 4 steps use the nibble tables (one Philox block -> 4
+// Bernoulli bits -> one table entry); the tail block walks step by step.
+// CONSTP: every suffix step has the same threshold thr0 (the BASELINE trees).
+template <unsigned KIND, bool CONSTP>
+__device__ __forceinline__ PathState walk_suffix(const McArgs& a, const Nib* __restrict__ nib, PathState st,
+                                                 uint32_t i, uint32_t stream, uint32_t rep, uint32_t thr0,
+                                                 bool all_up) {
   constexpr bool need_max = KIND == kFL;
   constexpr bool need_min = KIND == kFLP;
   constexpr bool need_sum = KIND == kAC || KIND == kAP;
   const int nsuf = a.N - a.r;
+  const int nfull = nsuf >> 2;
   uint32_t blk[4];
-  for (int j = 0; 4 * j < nsuf; ++j) {
+  auto up_of = [&](int w, uint32_t word) -> bool {
+    if (CONSTP) return (word < thr0) || all_up;
+    const int t = a.r + w;
+    return (word < a.thr[t]) || ((t < 32 ? (a.always[0] >> t) : (a.always[1] >> (t - 32))) & 1u);
+  };
+#pragma unroll 2
+  for (int j = 0; j < nfull; ++j) {
     philox4x32_10((uint32_t)j, i, stream, rep, a.key0, a.key1, blk);
+    const unsigned b = ((unsigned)up_of(4 * j, blk[0]) << 3) | ((unsigned)up_of(4 * j + 1, blk[1]) << 2) |
+                       ((unsigned)up_of(4 * j + 2, blk[2]) << 1) | (unsigned)up_of(4 * j + 3, blk[3]);
+    const Nib q = nib[b];
+    if (need_sum) st.sum = fma(st.S, q.c, st.sum);
+    if (need_max) st.mx = fmax(st.mx, st.S * q.x);
+    if (need_min) st.mn = fmin(st.mn, st.S * q.n);
+    st.S *= q.e;
+  }
+  if (4 * nfull < nsuf) {
+    philox4x32_10((uint32_t)nfull, i, stream, rep, a.key0, a.key1, blk);
 #pragma unroll
-    for (int l = 0; l < 4; ++l) {
-      const int w = 4 * j + l;
+    for (int l = 0; l < 3; ++l) {
+      const int w = 4 * nfull + l;
       if (w < nsuf) {
-        const int t = a.r + w;
-        const bool up = (blk[l] < a.thr[t]) || ((t < 32 ? (a.always[0] >> t) : (a.always[1] >> (t - 32))) & 1u);
-        st.S *= up ? a.u : a.d;
+        st.S *= up_of(w, blk[l]) ? a.u : a.d;
         if (need_sum) st.sum += st.S;
         if (need_max) st.mx = fmax(st.mx, st.S);
         if (need_min) st.mn = fmin(st.mn, st.S);
@@ -120,14 +163,38 @@ __device__ __forceinline__ PathState walk_suffix(const McArgs& a, PathState st, 
   return st;
 }
 
+// Per-thread running statistics without a per-draw division: sums of
+// (v - c) and (v - c)^2 around the thread's first value c (no cancellation
+// problem: c is an actual sample), turned into (n, mean, M2) once.
+struct ShiftedSums {
+  double c, s1, s2, n;
+  __device__ __forceinline__ void add(double v) {
+    if (n == 0.0) c = v;
+    const double d = v - c;
+    s1 += d;
+    s2 = fma(d, d, s2);
+    n += 1.0;
+  }
+  __device__ __forceinline__ Welford welford() const {
+    if (n == 0.0) return Welford{0.0, 0.0, 0.0};
+    const double m1 = s1 / n;
+    return Welford{n, c + m1, fmax(s2 - s1 * m1, 0.0)};
+  }
+};
+
 // ---------------------------------------------------------------------------
 // K4/K5: one CTA per work item (grid-stride).  item -> (rep k, stratum m, first draw)
-template <unsigned KIND>
+template <unsigned KIND, bool CONSTP>
 __global__ void __launch_bounds__(kMcThreads)
 k_mc_strata(const __grid_constant__ McArgs a, const unsigned long long* __restrict__ draws,
             const unsigned long long* __restrict__ item_stratum, const unsigned long long* __restrict__ item_first,
             unsigned long long items_per_rep, int n_reps, double* __restrict__ item_out) {
+  __shared__ Nib nib[16];
+  build_nib(a, nib);
+  __syncthreads();
   const unsigned long long n_items = items_per_rep * (unsigned long long)n_reps;
+  const uint32_t thr0 = a.thr[a.r < a.N ? a.r : 0];
+  const bool all_up = (a.always[0] | a.always[1]) != 0u;
   for (unsigned long long it = blockIdx.x; it < n_items; it += gridDim.x) {
     const unsigned long long k = it / items_per_rep, li = it % items_per_rep;
     const unsigned long long m = item_stratum[li];
@@ -135,16 +202,13 @@ k_mc_strata(const __grid_constant__ McArgs a, const unsigned long long* __restri
     const unsigned long long R = draws[m];
     const unsigned long long last = first + kChunk < R ? first + kChunk : R;
     const PathState pre = prefix_state(a, m);
-    Welford w{0.0, 0.0, 0.0};
+    ShiftedSums acc{0.0, 0.0, 0.0, 0.0};
     for (unsigned long long i = first + threadIdx.x; i < last; i += kMcThreads) {
-      const PathState st = walk_suffix<KIND>(a, pre, (uint32_t)i, (uint32_t)m, a.rep0 + (uint32_t)k);
-      const double v = payoff_of(KIND, st, a.K, a.N);
-      w.n += 1.0;
-      const double delta = v - w.mean;
-      w.mean += delta / w.n;
-      w.m2 = fma(delta, v - w.mean, w.m2);
+      const PathState st = walk_suffix<KIND, CONSTP>(a, nib, pre, (uint32_t)i, (uint32_t)m, a.rep0 + (uint32_t)k, thr0,
+                                                     all_up);
+      acc.add(payoff_of(KIND, st, a.K, a.N));
     }
-    const Welford t = cta_merge(w);
+    const Welford t = cta_merge(acc.welford());
     if (threadIdx.x == 0) {
       item_out[it * 3 + 0] = t.n;
       item_out[it * 3 + 1] = t.mean;
@@ -180,10 +244,24 @@ cudaError_t launch_mc_strata(const McArgs& a, const unsigned long long* draws_de
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const unsigned long long n_items = items_per_rep * (unsigned long long)n_reps;
+  bool constp = true;  // one threshold for every suffix step (and one p == 1 flag)
+  for (int t = a.r; t < a.N; ++t) constp = constp && a.thr[t] == a.thr[a.r];
+  {
+    const bool any = (a.always[0] | a.always[1]) != 0u;
+    for (int t = a.r; t < a.N && any; ++t)
+      constp = constp && (((t < 32 ? a.always[0] >> t : a.always[1] >> (t - 32)) & 1u) != 0u);
+  }
   if (n_items) {
     const int grid = (int)(n_items < (unsigned long long)sms * 16 ? n_items : (unsigned long long)sms * 16);
-#define BP_MC_CASE(K) \
-  case K: k_mc_strata<K><<<grid, kMcThreads, 0, st>>>(a, draws_dev, item_stratum_dev, item_first_dev, items_per_rep, n_reps, item_out_dev); break;
+#define BP_MC_CASE(K)                                                                                         \
+  case K:                                                                                                     \
+    if (constp)                                                                                               \
+      k_mc_strata<K, true><<<grid, kMcThreads, 0, st>>>(a, draws_dev, item_stratum_dev, item_first_dev,       \
+                                                         items_per_rep, n_reps, item_out_dev);                 \
+    else                                                                                                      \
+      k_mc_strata<K, false><<<grid, kMcThreads, 0, st>>>(a, draws_dev, item_stratum_dev, item_first_dev,      \
+                                                          items_per_rep, n_reps, item_out_dev);                \
+    break;
     switch (a.kind) {
       BP_MC_CASE(kEC) BP_MC_CASE(kEP) BP_MC_CASE(kAP) BP_MC_CASE(kFLP) BP_MC_CASE(kAC) BP_MC_CASE(kFL)
       default: return cudaErrorInvalidValue;
@@ -208,6 +286,9 @@ k_mc_shared(const __grid_constant__ McArgs a, unsigned long long R, const double
             const double* __restrict__ pre_tab /* [M][4] S, sum, mx, mn after r steps */, int M,
             unsigned long long items_per_rep, int n_reps, double* __restrict__ item_out,
             double* __restrict__ warp_sums /* [item][8][M] */) {
+  __shared__ Nib nib[16];
+  build_nib(a, nib);
+  __syncthreads();
   const unsigned long long n_items = items_per_rep * (unsigned long long)n_reps;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (unsigned long long it = blockIdx.x; it < n_items; it += gridDim.x) {
@@ -224,7 +305,7 @@ k_mc_shared(const __grid_constant__ McArgs a, unsigned long long R, const double
       const bool live = i < last;
       // suffix relative to a unit start price
       PathState rel{1.0, 0.0, -INFINITY, INFINITY};
-      if (live) rel = walk_suffix<KIND>(a, rel, (uint32_t)i, 0u, a.rep0 + (uint32_t)k);
+      if (live) rel = walk_suffix<KIND, false>(a, nib, rel, (uint32_t)i, 0u, a.rep0 + (uint32_t)k, 0u, false);
       double inner = 0.0;
       for (int m = 0; m < M; ++m) {
         const double S = pre_tab[4 * m], sum = pre_tab[4 * m + 1], mx = pre_tab[4 * m + 2], mn = pre_tab[4 * m + 3];

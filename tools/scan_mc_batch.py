@@ -44,5 +44,8 @@ def batch_config5(n=4096, N=24):
 
 
 if __name__ == "__main__":
-    mc_config4()
-    batch_config5()
+    which = sys.argv[1:] or ["mc", "batch"]
+    if "mc" in which:
+        mc_config4()
+    if "batch" in which:
+        batch_config5()
