@@ -1,19 +1,23 @@
 // K3: batched exact pricing -- many independent trees (same N), one payoff.
 //
 // The reference has no batch API; its callers loop value_exact_parallel over
-// requests (exact.py:112-133).  Here one CTA group owns one option: the CTA
-// builds that option's inner / middle tables and weights in shared memory
-// (each option has its own u, d, p), then runs the same affine-threshold
-// leaf block as K1 (bp_exact_kernels.cu) with the tables read from shared
-// memory (broadcast LDS), and reduces its partial in a fixed order.
+// requests (exact.py:112-133).  Here a group of CTAs owns one option: every
+// CTA builds that option's tables in shared memory (each option has its own
+// u, d, p) -- the inner table sorted inside each up-count class by a rank
+// computation, the group prefix sums, the middle tables and the weights --
+// and then runs the same explicit leaf block as K1 (bp_leaf.cuh) over its
+// share of the option's thread prefixes, nodes in pairs.  Partials are
+// reduced in a fixed order (CTA tree, then ascending CTA index per option).
 #include <cmath>
 #include "bp_kernels.h"
+#include "bp_leaf.cuh"
 
 namespace bp {
 
-constexpr int kBL = 8;             // inner bits
-constexpr int kBM = 6;             // middle bits
+constexpr int kBL = 8;   // inner bits
+constexpr int kBM = 6;   // middle bits
 constexpr int kBThreads = 256;
+constexpr int kBNP = 2;  // nodes per leaf block
 
 struct BatchArgs {
   int N;
@@ -21,23 +25,20 @@ struct BatchArgs {
   int cpo_log2;  // CTAs per option = 2^cpo_log2
 };
 
-__device__ __forceinline__ double bu32_to_double(unsigned x) {
-  return __hiloint2double(0x43300000, (int)x) - 4503599627370496.0;
-}
-
 template <unsigned KIND>
-__global__ void __launch_bounds__(kBThreads)
+__global__ void __launch_bounds__(kBThreads, 3)
 k_exact_batch(const BatchOption* __restrict__ opts, BatchArgs ba, double2* __restrict__ partial) {
-  constexpr int NL = 1 << kBL, NC = kBL + 1, NMID = 1 << kBM;
+  constexpr int NL = 1 << kBL, NC = kBL + 1, NMID = 1 << kBM, NG = n_groups(kBL), NP = kBNP;
   constexpr bool AC = KIND == kAC, AP = KIND == kAP, FL = KIND == kFL, FLP = KIND == kFLP, EC = KIND == kEC,
                  EP = KIND == kEP;
   constexpr bool TAB = AC || AP || FL || FLP;
+  constexpr bool DESC = AC || FL;  // compare direction '>' -> sort descending
   __shared__ __align__(16) double tab[NL];
+  __shared__ double gpre[NG * kGroupSlots];
   __shared__ double mid_c[NMID], mid_e[NMID], mid_x[NMID];
   __shared__ int mid_h[NMID];
   __shared__ double w[kMaxN + 2 + NC];
   __shared__ double e_cls[NC], b_cls[NC];
-  __shared__ double s_up, s_dn;
   __shared__ double red_s[kBThreads], red_c[kBThreads];
 
   const int opt = blockIdx.x >> ba.cpo_log2;
@@ -46,17 +47,34 @@ k_exact_batch(const BatchOption* __restrict__ opts, BatchArgs ba, double2* __res
   const int N = ba.N, D = N - kBL, Dp = D - kBM;
   const int tid = threadIdx.x;
 
-  // ---- per-option tables (the walk of csrc/bp_capi.cu build_inner)
-  for (int s = tid; s < NL; s += kBThreads) {
+  // ---- inner table: value of leaf s, then its position (class-major, sorted
+  // in the compare direction inside the class; ties by leaf index)
+  double v = 0.0;
+  if (TAB && tid < NL) {
     double r = 1.0, c = 0.0, mx = 0.0, mn = INFINITY;
     for (int j = 0; j < kBL; ++j) {
-      r *= ((s >> (kBL - 1 - j)) & 1) ? o.u : o.d;
+      r *= ((tid >> (kBL - 1 - j)) & 1) ? o.u : o.d;
       c += r;
       mx = fmax(mx, r);
       mn = fmin(mn, r);
     }
-    tab[s] = (AC || AP) ? c : FL ? mx : mn;
+    v = (AC || AP) ? c : FL ? mx : mn;
+    tab[tid] = v;
   }
+  __syncthreads();
+  int pos = -1;
+  if (TAB && tid < NL) {
+    const int cls = __popc(tid);
+    int rank = 0;
+    for (int s2 = 0; s2 < NL; ++s2) {
+      if (__popc(s2) != cls) continue;
+      const double v2 = tab[s2];
+      rank += DESC ? (v2 > v || (v2 == v && s2 < tid)) : (v2 < v || (v2 == v && s2 < tid));
+    }
+    pos = class_start(kBL, cls) + rank;
+  }
+  __syncthreads();
+  if (pos >= 0) tab[pos] = v;
   for (int j = tid; j < NMID; j += kBThreads) {
     double r = 1.0, c = 0.0, mx = 0.0, mn = INFINITY;
     int h = 0;
@@ -76,32 +94,35 @@ k_exact_batch(const BatchOption* __restrict__ opts, BatchArgs ba, double2* __res
   for (int h = tid; h < kMaxN + 2 + NC; h += kBThreads)
     w[h] = (h <= N) ? o.disc * pow(o.p, (double)h) * pow(1.0 - o.p, (double)(N - h)) : 0.0;
   if (tid < NC) {
-    double r = 1.0, b = 1.0;
+    double r = 1.0;
     for (int j = 0; j < tid; ++j) r *= o.u;
     for (int j = tid; j < kBL; ++j) r *= o.d;
-    for (int j = 0; j < tid; ++j) b = b * (kBL - j) / (j + 1);
     e_cls[tid] = r;
-    b_cls[tid] = rint(b);
+    b_cls[tid] = (double)binom(kBL, tid);
   }
   __syncthreads();
-  if (tid == 0) {
-    // tables are increasing in every up bit when u > d: the minimum is entry 0
-    int e = 0;
-    frexp(tab[0], &e);
-    s_up = ldexp(1.0, 1 - e);
-    s_dn = ldexp(1.0, kMaskExp - (1 - e));
-  }
-  __syncthreads();
-  for (int s = tid; s < NL; s += kBThreads) tab[s] *= s_up;
+  // group prefix sums (compensated, rounded once), one (group, n) per thread
+  if (TAB)
+    for (int gi = tid; gi < NG * kGroupSlots; gi += kBThreads) {
+      const int g = gi / kGroupSlots, n = gi % kGroupSlots;
+      int cls = 0;
+      while (cls < kBL && group_base(kBL, cls + 1) <= g) ++cls;
+      const int gl = g - group_base(kBL, cls);
+      const int len = min(kGroup, binom(kBL, cls) - kGroup * gl);
+      const int i0 = class_start(kBL, cls) + kGroup * gl;
+      double s = 0.0, cc = 0.0;
+      for (int k = 0; k < n && k < len; ++k) comp_add(s, cc, tab[i0 + k]);
+      gpre[gi] = s + cc;
+    }
   __syncthreads();
 
   const double NK = (double)N * o.K;
-  const int zlo = tid & (ba.N >> 10);  // 0 (N < 1024), opaque to the compiler
   const double INF = __longlong_as_double(0x7ff0000000000000ll);
   double ts = 0.0, tc = 0.0;
   const unsigned long long n_pre = 1ull << Dp;
   const unsigned long long per = n_pre >> ba.cpo_log2;
   const unsigned long long p0 = (unsigned long long)part * per;
+  const int zero = (N >> 10) & tid;  // 0, opaque to the compiler
   for (unsigned long long pi = p0 + tid; pi < p0 + per; pi += kBThreads) {
     double S = o.S0, Sig = 0.0, X = FL ? 0.0 : INF;
     int h = 0;
@@ -113,57 +134,41 @@ k_exact_batch(const BatchOption* __restrict__ opts, BatchArgs ba, double2* __res
       if (FLP) X = fmin(X, S);
       h += b;
     }
-    for (int j = 0; j < NMID; ++j) {
-      const double Sn = S * mid_e[j];
-      const double Sg = fma(S, mid_c[j], Sig);
-      const double Xn = FL ? fmax(X, S * mid_x[j]) : FLP ? fmin(X, S * mid_x[j]) : 0.0;
-      const int hn = h + mid_h[j];
-      const double base = Sg - NK;
-      double th = 0.0;
-      if (AC || AP) th = (-base / Sn) * s_up;
-      if (FL) th = (Xn / Sn) * s_up;
-      if (FLP) th = (fmin(Xn, o.K) / Sn) * s_up;
-      double acc[NC];
-      unsigned cnt[NC];
+    for (int j0 = 0; j0 < NMID; j0 += NP) {
+      double Sn[NP], Xn[NP], base[NP], th[NP];
+      int hn[NP];
 #pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        acc[c] = 0.0;
-        cnt[c] = 0u;
+      for (int p = 0; p < NP; ++p) {
+        const int j = j0 + p;
+        Sn[p] = S * mid_e[j];
+        const double Sg = fma(S, mid_c[j], Sig);
+        Xn[p] = FL ? fmax(X, S * mid_x[j]) : FLP ? fmin(X, S * mid_x[j]) : 0.0;
+        hn[p] = h + mid_h[j];
+        base[p] = Sg - NK;
+        const double rS = 1.0 / Sn[p];
+        th[p] = (AC || AP) ? -base[p] * rS : FL ? Xn[p] * rS : FLP ? fmin(Xn[p], o.K) * rS : 0.0;
       }
-      if (TAB) {
-        const double2* tb = reinterpret_cast<const double2*>(tab) + (j & zlo);
+      double acc[NP][NC];
+      int cnt[NP][NC];
+      zero_acc<NP, NC>(acc, cnt);
+      if (TAB) leaf_block<kBL, NP, 0, DESC>(reinterpret_cast<const double2*>(tab) + (j0 & zero), gpre, th, acc, cnt);
 #pragma unroll
-        for (int s2 = 0; s2 < NL / 2; ++s2) {
-          const double2 v = tb[s2];
+      for (int p = 0; p < NP; ++p) {
+        double val = 0.0;
 #pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {
-            const int s = 2 * s2 + hh;
-            const int cls = __popc(s);
-            const double c = hh ? v.y : v.x;
-            const bool itm = (AC || FL) ? (c > th) : (c < th);
-            const unsigned mh = itm ? kMaskHi : 0u;
-            acc[cls] = fma(__hiloint2double((int)mh, zlo), c, acc[cls]);
-            cnt[cls] += mh;
-          }
+        for (int c = 0; c < NC; ++c) {
+          const double n = (double)cnt[p][c], bc = b_cls[c];
+          double contrib = 0.0;
+          if (AC) contrib = fma(Sn[p], acc[p][c], base[p] * n);
+          if (AP) contrib = fma(-Sn[p], acc[p][c], -base[p] * n);
+          if (FL) contrib = fma(-Sn[p] * e_cls[c], bc, fma(Sn[p], acc[p][c], Xn[p] * (bc - n)));
+          if (FLP) contrib = fma(bc - n, fmax(o.K - Xn[p], 0.0), fma(o.K, n, -Sn[p] * acc[p][c]));
+          if (EC) contrib = bc * fmax(fma(Sn[p], e_cls[c], -o.K), 0.0);
+          if (EP) contrib = bc * fmax(fma(-Sn[p], e_cls[c], o.K), 0.0);
+          val = fma(w[hn[p] + c], contrib, val);
         }
+        comp_add(ts, tc, val);
       }
-      double v = 0.0;
-#pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        const double wv = w[hn + c];
-        const double bc = b_cls[c];
-        const double A = acc[c] * s_dn;
-        const double n = bu32_to_double(cnt[c] >> 24);
-        double contrib = 0.0;
-        if (AC) contrib = fma(Sn, A, base * n);
-        if (AP) contrib = fma(-Sn, A, -base * n);
-        if (FL) contrib = fma(-Sn * e_cls[c], bc, fma(Sn, A, Xn * (bc - n)));
-        if (FLP) contrib = fma(bc - n, fmax(o.K - Xn, 0.0), fma(o.K, n, -Sn * A));
-        if (EC) contrib = bc * fmax(fma(Sn, e_cls[c], -o.K), 0.0);
-        if (EP) contrib = bc * fmax(fma(-Sn, e_cls[c], o.K), 0.0);
-        v = fma(wv, contrib, v);
-      }
-      comp_add(ts, tc, v);
     }
   }
   // fixed-order CTA reduce
@@ -197,9 +202,9 @@ __global__ void k_batch_combine(const double2* __restrict__ partial, int n_opts,
 }
 
 int batch_ctas_per_option(int n_opts) {
-  // enough CTAs to fill 148 SMs x 4 resident CTAs, at most 16 per option
+  // enough CTAs to fill 148 SMs x 3 resident CTAs, at most 16 per option
   int l = 0;
-  while (l < 4 && (long long)n_opts << l < 148 * 4) ++l;
+  while (l < 4 && (long long)n_opts << l < 148 * 3) ++l;
   return l;
 }
 

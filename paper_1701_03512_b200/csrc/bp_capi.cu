@@ -804,7 +804,7 @@ extern "C" int bp_exact_batch(const bp_tree* trees, int n_opts, uint32_t payoff,
       cudaStreamDestroy(s);
     }
   } sg{st};
-  const int cpo = batch_ctas_per_option(n_opts);
+  const int cpo = std::min(batch_ctas_per_option(n_opts), N - 14);  // >= 1 prefix per CTA
   DevBuf<BatchOption> d_o;
   DevBuf<double> d_v;
   DevBuf<double2> d_p;
