@@ -432,60 +432,68 @@ struct DeviceJob {
   std::string err;
 };
 
+// Per-device resources kept across calls (stream, events, result buffers,
+// pinned staging) so a synchronous valuation costs launches + one copy, not
+// stream/event creation and allocations.  One call per device at a time.
+struct DevCtx {
+  std::mutex mu;
+  bool ready = false;
+  cudaStream_t st = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  double* out_dev = nullptr;               // kMaxSB * 6 * 2
+  unsigned long long* hist_dev = nullptr;  // 66
+  double* out_host = nullptr;              // pinned
+  unsigned long long* hist_host = nullptr; // pinned
+};
+static DevCtx g_ctx[64];
+
+static cudaError_t ctx_init(DevCtx& c, int dev) {
+  if (c.ready) return cudaSuccess;
+  cudaError_t e;
+  if ((e = cudaSetDevice(dev)) != cudaSuccess) return e;
+  if ((e = cudaStreamCreateWithFlags(&c.st, cudaStreamNonBlocking)) != cudaSuccess) return e;
+  if ((e = cudaEventCreate(&c.e0)) != cudaSuccess) return e;
+  if ((e = cudaEventCreate(&c.e1)) != cudaSuccess) return e;
+  if ((e = cudaMalloc((void**)&c.out_dev, sizeof(double) * kMaxSB * BP_N_PAYOFFS * 2)) != cudaSuccess) return e;
+  if ((e = cudaMalloc((void**)&c.hist_dev, sizeof(unsigned long long) * 66)) != cudaSuccess) return e;
+  if ((e = cudaMallocHost((void**)&c.out_host, sizeof(double) * kMaxSB * BP_N_PAYOFFS * 2)) != cudaSuccess) return e;
+  if ((e = cudaMallocHost((void**)&c.hist_host, sizeof(unsigned long long) * 66)) != cudaSuccess) return e;
+  c.ready = true;
+  return cudaSuccess;
+}
+
 static void run_device_job(const bp_tree* t, uint32_t payoffs, uint32_t flags, DeviceJob* job) {
-  auto setrc = [&](int rc) {
-    job->rc = rc;
-    job->err = g_err;
-  };
   auto cuda_fail = [&](cudaError_t e, const char* what) {
     job->rc = BP_E_CUDA;
     job->err = std::string("CUDA error ") + cudaGetErrorString(e) + " (" + what + ")";
   };
+  if (job->device < 0 || job->device >= 64) return cuda_fail(cudaErrorInvalidDevice, "device index");
+  DevCtx& c = g_ctx[job->device];
+  std::lock_guard<std::mutex> lock(c.mu);
   cudaError_t e = cudaSetDevice(job->device);
   if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
-  cudaStream_t st;
-  if ((e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)) != cudaSuccess) return cuda_fail(e, "stream");
-  double* out = nullptr;
-  unsigned long long* hist = nullptr;
-  cudaEvent_t e0, e1;
-  cudaEventCreate(&e0);
-  cudaEventCreate(&e1);
+  if ((e = ctx_init(c, job->device)) != cudaSuccess) return cuda_fail(e, "device context");
   const bool cnt = (flags & BP_FLAG_COUNT) != 0;
-  job->partials.assign((size_t)job->sb_count * BP_N_PAYOFFS * 2, 0.0);
+  const size_t np = (size_t)job->sb_count * BP_N_PAYOFFS * 2;
+  job->partials.assign(np, 0.0);
   job->hist.assign(66, 0ull);
-  do {
-    if ((e = cudaMallocAsync((void**)&out, sizeof(double) * job->partials.size(), st)) != cudaSuccess) {
-      cuda_fail(e, "alloc");
-      break;
-    }
-    if (cnt) {
-      if ((e = cudaMallocAsync((void**)&hist, sizeof(unsigned long long) * 66, st)) != cudaSuccess) {
-        cuda_fail(e, "alloc");
-        break;
-      }
-      cudaMemsetAsync(hist, 0, sizeof(unsigned long long) * 66, st);
-    }
-    cudaEventRecord(e0, st);
-    int rc = enqueue_superblocks(t, payoffs, flags, job->device, job->sb_first, job->sb_count, out, hist, st);
-    if (rc) {
-      setrc(rc);
-      break;
-    }
-    cudaEventRecord(e1, st);
-    cudaMemcpyAsync(job->partials.data(), out, sizeof(double) * job->partials.size(), cudaMemcpyDeviceToHost, st);
-    if (cnt) cudaMemcpyAsync(job->hist.data(), hist, sizeof(unsigned long long) * 66, cudaMemcpyDeviceToHost, st);
-    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) {
-      cuda_fail(e, "valuation");
-      break;
-    }
-    cudaEventElapsedTime(&job->ms, e0, e1);
-  } while (0);
-  if (out) cudaFreeAsync(out, st);
-  if (hist) cudaFreeAsync(hist, st);
-  cudaStreamSynchronize(st);
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-  cudaStreamDestroy(st);
+  if (cnt) cudaMemsetAsync(c.hist_dev, 0, sizeof(unsigned long long) * 66, c.st);
+  cudaEventRecord(c.e0, c.st);
+  int rc = enqueue_superblocks(t, payoffs, flags, job->device, job->sb_first, job->sb_count, c.out_dev,
+                               cnt ? c.hist_dev : nullptr, c.st);
+  if (rc) {
+    job->rc = rc;
+    job->err = g_err;
+    cudaStreamSynchronize(c.st);
+    return;
+  }
+  cudaEventRecord(c.e1, c.st);
+  cudaMemcpyAsync(c.out_host, c.out_dev, sizeof(double) * np, cudaMemcpyDeviceToHost, c.st);
+  if (cnt) cudaMemcpyAsync(c.hist_host, c.hist_dev, sizeof(unsigned long long) * 66, cudaMemcpyDeviceToHost, c.st);
+  if ((e = cudaStreamSynchronize(c.st)) != cudaSuccess) return cuda_fail(e, "valuation");
+  std::memcpy(job->partials.data(), c.out_host, sizeof(double) * np);
+  if (cnt) std::memcpy(job->hist.data(), c.hist_host, sizeof(unsigned long long) * 66);
+  cudaEventElapsedTime(&job->ms, c.e0, c.e1);
 }
 
 extern "C" int bp_exact(const bp_tree* tree, uint32_t payoffs, uint32_t flags, int n_dev, const int* devices,
