@@ -121,6 +121,21 @@ int bp_exact_superblocks(const bp_tree* tree, uint32_t payoffs, uint32_t flags,
                          int device, int sb_first, int sb_count,
                          double* out_dev, uint64_t* hist_dev, void* stream);
 
+/* A prepared valuation (kernel arguments and tables built once, scratch
+ * reused): for repeated valuations of one tree, e.g. one step per rank in a
+ * one-process-per-GPU job.  Enqueue has the semantics of
+ * bp_exact_superblocks; calls on one plan and device must use one stream.
+ * Replaces the per-call setup of _rank_value (exact.py:83-100).            */
+typedef struct bp_exact_plan bp_exact_plan;
+int bp_exact_plan_create(const bp_tree* tree, uint32_t payoffs, uint32_t flags,
+                         bp_exact_plan** plan);
+int bp_exact_plan_layout(const bp_exact_plan* plan, int* n_superblocks,
+                         int* engine, int* inner_bits);
+int bp_exact_plan_enqueue(bp_exact_plan* plan, int device, int sb_first,
+                          int sb_count, double* out_dev, uint64_t* hist_dev,
+                          void* stream);
+void bp_exact_plan_destroy(bp_exact_plan* plan);
+
 /* Fixed-order (ascending super-block) compensated combination of the
  * gathered partials (host memory, n_sb * BP_N_PAYOFFS * 2 doubles) into
  * the discounted values (BP_N_PAYOFFS doubles).                            */

@@ -69,7 +69,8 @@ class BpExactResult(ctypes.Structure):
 EXPORTED = (
     "bp_exact", "bp_exact_layout", "bp_exact_superblocks", "bp_combine_superblocks", "bp_exact_batch",
     "bp_mc_strata", "bp_mc_shared", "bp_philox4x32_10", "bp_fp64_peak", "bp_device_count",
-    "bp_abi_version", "bp_last_error",
+    "bp_abi_version", "bp_last_error", "bp_exact_plan_create", "bp_exact_plan_layout", "bp_exact_plan_enqueue",
+    "bp_exact_plan_destroy",
 )
 
 _lib = None
@@ -102,6 +103,12 @@ def _declare(L):
     L.bp_exact_layout.argtypes = [P(BpTree), c_u32, c_u32, P(c_int), P(c_int), P(c_int)]
     L.bp_exact_superblocks.argtypes = [P(BpTree), c_u32, c_u32, c_int, c_int, c_int, ctypes.c_void_p,
                                        ctypes.c_void_p, ctypes.c_void_p]
+    L.bp_exact_plan_create.argtypes = [P(BpTree), c_u32, c_u32, P(ctypes.c_void_p)]
+    L.bp_exact_plan_layout.argtypes = [ctypes.c_void_p, P(c_int), P(c_int), P(c_int)]
+    L.bp_exact_plan_enqueue.argtypes = [ctypes.c_void_p, c_int, c_int, c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                        ctypes.c_void_p]
+    L.bp_exact_plan_destroy.argtypes = [ctypes.c_void_p]
+    L.bp_exact_plan_destroy.restype = None
     L.bp_combine_superblocks.argtypes = [P(c_dbl), c_int, c_u32, P(c_dbl)]
     L.bp_exact_batch.argtypes = [P(BpTree), c_int, c_u32, c_int, P(c_dbl), P(c_dbl)]
     L.bp_mc_strata.argtypes = [P(BpTree), c_u32, c_int, P(c_u64), c_u64, c_u32, c_u32, c_int, P(c_dbl),
@@ -117,7 +124,7 @@ def _declare(L):
     L.bp_last_error.restype = ctypes.c_char_p
     for name in EXPORTED:
         fn = getattr(L, name)
-        if name not in ("bp_philox4x32_10", "bp_last_error"):
+        if name not in ("bp_philox4x32_10", "bp_last_error", "bp_exact_plan_destroy"):
             fn.restype = c_int
 
 

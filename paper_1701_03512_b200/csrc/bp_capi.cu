@@ -329,42 +329,47 @@ static int device_sm_count(int dev) {
 
 // Enqueue the valuation of super-blocks [sb_first, sb_first+sb_count) on
 // the current device.  out_dev: [sb_count][6][2] doubles (device).
-static int enqueue_superblocks(const bp_tree* t, uint32_t payoffs, uint32_t flags, int dev, int sb_first,
-                               int sb_count, double* out_dev, unsigned long long* hist_dev, cudaStream_t st) {
-  const Layout lay = choose_layout(t, payoffs, flags, nullptr);
-  if (sb_first < 0 || sb_count < 1 || sb_first + sb_count > lay.n_sb)
-    return fail(BP_E_RANK_RANGE, "super-block range [" + std::to_string(sb_first) + ", " +
-                                     std::to_string(sb_first + sb_count) + ") outside [0, " +
-                                     std::to_string(lay.n_sb) + ")");
-  const bool cnt = (flags & BP_FLAG_COUNT) != 0;
-  if (cnt && !hist_dev) return fail(BP_E_INVALID_INPUT, "BP_FLAG_COUNT needs a histogram buffer");
-  const unsigned long long u0 = (unsigned long long)sb_first * lay.units_per_sb;
-  const unsigned long long u1 = u0 + (unsigned long long)sb_count * lay.units_per_sb;
-  const unsigned long long n_units = u1 - u0;
-  keep_pool(dev);
-  double2* unit_out = nullptr;
-  BP_CUDA(cudaMallocAsync((void**)&unit_out, sizeof(double2) * kNumKinds * n_units, st));
-  // kernels index unit_out by absolute unit; shift the base pointer
-  double2* unit_base = unit_out - (ptrdiff_t)(u0 * kNumKinds);
-  BP_CUDA(cudaMemsetAsync(out_dev, 0, sizeof(double) * 2 * kNumKinds * sb_count, st));
-  const int sms = device_sm_count(dev);
+// ---------------------------------------------------------------------------
+// A prepared valuation: layout, prebuilt kernel arguments per kind group and
+// per-device scratch.  Building the tables costs host time (sorting, pow);
+// a plan does it once so repeated launches are launches only.
+struct bp_exact_plan {
+  bp_tree tree;
+  std::vector<double> probs;
+  uint32_t payoffs = 0, flags = 0;
+  Layout lay{};
+  struct Group {
+    unsigned km;
+    std::vector<unsigned char> args;
+  };
+  std::vector<Group> groups;
+  GenericArgs gen{};
+  struct Scratch {
+    double2* p = nullptr;
+    size_t bytes = 0;
+  };
+  Scratch scratch[64];
+  std::mutex mu;
+};
+
+static int plan_build(const bp_tree* t, uint32_t payoffs, uint32_t flags, bp_exact_plan* P) {
+  P->probs.assign(t->up_probs, t->up_probs + t->n_steps);
+  P->tree = *t;
+  P->tree.up_probs = P->probs.data();
+  P->payoffs = payoffs;
+  P->flags = flags;
+  P->lay = choose_layout(t, payoffs, flags, nullptr);
+  const Layout& lay = P->lay;
   if (lay.engine == 1) {
-    bool first_group = true;  // bookkeeping once per valuation, not per kind group
     for (unsigned km : fast_groups(payoffs)) {
-      const bool cnt_g = cnt && first_group;
-      first_group = false;
-      std::vector<unsigned char> buf;
-      int rc = build_fast_args(t, lay, km, buf);
+      bp_exact_plan::Group g;
+      g.km = km;
+      int rc = build_fast_args(&P->tree, lay, km, g.args);
       if (rc) return rc;
-      set_units(buf, lay.L, u0, u1);
-      const int occ = std::max(1, occupancy_exact_fast(lay.L, km, cnt_g));
-      const unsigned long long want = (n_units + 7) / 8;
-      const int grid = (int)std::max<unsigned long long>(1, std::min<unsigned long long>(want, (unsigned long long)occ * sms));
-      BP_CUDA(launch_exact_fast(lay.L, km, buf.data(), cnt_g, grid, st, unit_base, hist_dev));
-      BP_CUDA(launch_sb_reduce(unit_base, lay.units_per_sb, sb_first, sb_count, km, 1.0 / t->n_steps, out_dev, st));
+      P->groups.push_back(std::move(g));
     }
   } else {
-    GenericArgs g{};
+    GenericArgs& g = P->gen;
     g.S0 = t->S0;
     g.K = t->K;
     g.u = t->u;
@@ -375,17 +380,132 @@ static int enqueue_superblocks(const bp_tree* t, uint32_t payoffs, uint32_t flag
     g.N = t->n_steps;
     g.g = lay.g;
     g.kinds = payoffs;
+    g.n_codes = 1ull << t->n_steps;
+  }
+  return BP_OK;
+}
+
+// Enqueue the valuation of super-blocks [sb_first, sb_first+sb_count) on
+// device `dev` (current).  out_dev: [sb_count][6][2] doubles (device).
+// The plan's scratch for `dev` is reused: calls on one plan and device must
+// be issued on one stream (stream order protects the reuse).
+static int plan_enqueue(bp_exact_plan* P, int dev, int sb_first, int sb_count, double* out_dev,
+                        unsigned long long* hist_dev, cudaStream_t st) {
+  const Layout& lay = P->lay;
+  if (sb_first < 0 || sb_count < 1 || sb_first + sb_count > lay.n_sb)
+    return fail(BP_E_RANK_RANGE, "super-block range [" + std::to_string(sb_first) + ", " +
+                                     std::to_string(sb_first + sb_count) + ") outside [0, " +
+                                     std::to_string(lay.n_sb) + ")");
+  if (dev < 0 || dev >= 64) return fail(BP_E_NO_DEVICE, "device index out of range");
+  const bool cnt = (P->flags & BP_FLAG_COUNT) != 0;
+  if (cnt && !hist_dev) return fail(BP_E_INVALID_INPUT, "BP_FLAG_COUNT needs a histogram buffer");
+  const unsigned long long u0 = (unsigned long long)sb_first * lay.units_per_sb;
+  const unsigned long long u1 = u0 + (unsigned long long)sb_count * lay.units_per_sb;
+  const unsigned long long n_units = u1 - u0;
+  double2* unit_out = nullptr;
+  {
+    std::lock_guard<std::mutex> g(P->mu);
+    auto& sc = P->scratch[dev];
+    const size_t need = sizeof(double2) * kNumKinds * n_units;
+    if (sc.bytes < need) {
+      if (sc.p) cudaFreeAsync(sc.p, st);
+      sc.p = nullptr;
+      sc.bytes = 0;
+      BP_CUDA(cudaMallocAsync((void**)&sc.p, need, st));
+      sc.bytes = need;
+    }
+    unit_out = sc.p;
+  }
+  // kernels index unit_out by absolute unit; shift the base pointer
+  double2* unit_base = unit_out - (ptrdiff_t)(u0 * kNumKinds);
+  BP_CUDA(cudaMemsetAsync(out_dev, 0, sizeof(double) * 2 * kNumKinds * sb_count, st));
+  const int sms = device_sm_count(dev);
+  const unsigned long long want = (n_units + 7) / 8;
+  if (lay.engine == 1) {
+    bool first_group = true;  // bookkeeping once per valuation, not per kind group
+    for (auto& g : P->groups) {
+      const bool cnt_g = cnt && first_group;
+      first_group = false;
+      set_units(g.args, lay.L, u0, u1);
+      const int occ = std::max(1, occupancy_exact_fast(lay.L, g.km, cnt_g));
+      const int grid = (int)std::max<unsigned long long>(1, std::min<unsigned long long>(want, (unsigned long long)occ * sms));
+      BP_CUDA(launch_exact_fast(lay.L, g.km, g.args.data(), cnt_g, grid, st, unit_base, hist_dev));
+      BP_CUDA(launch_sb_reduce(unit_base, lay.units_per_sb, sb_first, sb_count, g.km, 1.0 / P->tree.n_steps,
+                               out_dev, st));
+    }
+  } else {
+    GenericArgs g = P->gen;
     g.unit_first = u0;
     g.unit_end = u1;
-    g.n_codes = 1ull << t->n_steps;
     const int occ = std::max(1, occupancy_exact_generic(cnt));
-    const unsigned long long want = (n_units + 7) / 8;
     const int grid = (int)std::max<unsigned long long>(1, std::min<unsigned long long>(want, (unsigned long long)occ * sms));
     BP_CUDA(launch_exact_generic(g, cnt, grid, st, unit_base, hist_dev));
-    BP_CUDA(launch_sb_reduce(unit_base, lay.units_per_sb, sb_first, sb_count, payoffs, 1.0, out_dev, st));
+    BP_CUDA(launch_sb_reduce(unit_base, lay.units_per_sb, sb_first, sb_count, P->payoffs, 1.0, out_dev, st));
   }
-  BP_CUDA(cudaFreeAsync(unit_out, st));
   return BP_OK;
+}
+
+static void plan_release_scratch(bp_exact_plan* P, cudaStream_t st) {
+  for (int d = 0; d < 64; ++d)
+    if (P->scratch[d].p) {
+      int cur = 0;
+      cudaGetDevice(&cur);
+      cudaSetDevice(d);
+      cudaFreeAsync(P->scratch[d].p, d == cur ? st : 0);
+      cudaSetDevice(cur);
+      P->scratch[d].p = nullptr;
+      P->scratch[d].bytes = 0;
+    }
+}
+
+static int enqueue_superblocks(const bp_tree* t, uint32_t payoffs, uint32_t flags, int dev, int sb_first,
+                               int sb_count, double* out_dev, unsigned long long* hist_dev, cudaStream_t st) {
+  keep_pool(dev);
+  bp_exact_plan P;
+  int rc = plan_build(t, payoffs, flags, &P);
+  if (rc) return rc;
+  rc = plan_enqueue(&P, dev, sb_first, sb_count, out_dev, hist_dev, st);
+  if (P.scratch[dev].p) cudaFreeAsync(P.scratch[dev].p, st);  // stream-ordered: after the kernels
+  P.scratch[dev].p = nullptr;
+  return rc;
+}
+
+extern "C" int bp_exact_plan_create(const bp_tree* tree, uint32_t payoffs, uint32_t flags, bp_exact_plan** out) {
+  int rc = validate_tree(tree, 62);
+  if (rc) return rc;
+  if ((rc = kinds_ok(payoffs))) return rc;
+  if (!out) return fail(BP_E_INVALID_INPUT, "plan pointer is NULL");
+  auto* P = new bp_exact_plan();
+  if ((rc = plan_build(tree, payoffs, flags, P))) {
+    delete P;
+    return rc;
+  }
+  *out = P;
+  return BP_OK;
+}
+
+extern "C" int bp_exact_plan_layout(const bp_exact_plan* plan, int* n_superblocks, int* engine, int* inner_bits) {
+  if (!plan) return fail(BP_E_INVALID_INPUT, "plan is NULL");
+  if (n_superblocks) *n_superblocks = plan->lay.n_sb;
+  if (engine) *engine = plan->lay.engine;
+  if (inner_bits) *inner_bits = plan->lay.L;
+  return BP_OK;
+}
+
+extern "C" int bp_exact_plan_enqueue(bp_exact_plan* plan, int device, int sb_first, int sb_count, double* out_dev,
+                                     uint64_t* hist_dev, void* stream) {
+  if (!plan) return fail(BP_E_INVALID_INPUT, "plan is NULL");
+  if (device < 0 || device >= bp_device_count()) return fail(BP_E_NO_DEVICE, "no CUDA device " + std::to_string(device));
+  BP_CUDA(cudaSetDevice(device));
+  keep_pool(device);
+  return plan_enqueue(plan, device, sb_first, sb_count, out_dev, reinterpret_cast<unsigned long long*>(hist_dev),
+                      static_cast<cudaStream_t>(stream));
+}
+
+extern "C" void bp_exact_plan_destroy(bp_exact_plan* plan) {
+  if (!plan) return;
+  plan_release_scratch(plan, 0);
+  delete plan;
 }
 
 extern "C" int bp_exact_layout(const bp_tree* tree, uint32_t payoffs, uint32_t flags, int* n_superblocks,

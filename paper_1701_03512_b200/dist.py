@@ -81,9 +81,12 @@ class ShardedExact:
 
         self.tree, self._keep, self.mask, self.flags = tree, keep, mask, flags
         self.rank, self.world, self.device = rank, world, device
+        # prepared plan: tables built once, scratch reused across steps
+        self._plan = ctypes.c_void_p()
+        _native.check(_native.lib().bp_exact_plan_create(ctypes.byref(tree), mask, flags, ctypes.byref(self._plan)))
         n_sb, eng, L = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
-        _native.check(_native.lib().bp_exact_layout(ctypes.byref(tree), mask, flags, ctypes.byref(n_sb),
-                                                    ctypes.byref(eng), ctypes.byref(L)))
+        _native.check(_native.lib().bp_exact_plan_layout(self._plan, ctypes.byref(n_sb), ctypes.byref(eng),
+                                                         ctypes.byref(L)))
         self.n_sb, self.engine, self.inner_bits = n_sb.value, eng.value, L.value
         self.first, self.count = shard_range(self.n_sb, rank, world)
         self.local = torch.zeros((self.count, N_PAYOFFS, 2), dtype=torch.float64, device=f"cuda:{device}")
@@ -93,9 +96,22 @@ class ShardedExact:
         import torch
 
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
-        _native.check(_native.lib().bp_exact_superblocks(
-            ctypes.byref(self.tree), self.mask, self.flags, self.device, self.first, self.count,
-            ctypes.c_void_p(self.local.data_ptr()), None, ctypes.c_void_p(st.cuda_stream)))
+        _native.check(_native.lib().bp_exact_plan_enqueue(
+            self._plan, self.device, self.first, self.count, ctypes.c_void_p(self.local.data_ptr()), None,
+            ctypes.c_void_p(st.cuda_stream)))
+
+    def close(self):
+        if self._plan:
+            import torch
+            torch.cuda.synchronize(self.device)
+            _native.lib().bp_exact_plan_destroy(self._plan)
+            self._plan = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
     def exchange(self, group=None):
         self.gathered = gather_partials(self.local, self.world, group) if self.world > 1 else self.local
