@@ -151,3 +151,36 @@ def test_variance_reduction_ratio_consistent_with_reference(N):
     # 10-rep means is known to a few per cent; allow 15 %
     assert ratio == pytest.approx(ref["ratio_basic_over_equal"], rel=0.15), (ratio, ref["ratio_basic_over_equal"])
     assert b.mean_value == pytest.approx(ref["basic"]["mean_value"], abs=6 * math.sqrt(b.mean_variance))
+
+
+def test_per_step_probabilities_and_N64_match_oracle():
+    """Non-constant per-step probabilities (with_custom_probs, model.py:152-161)
+    take the general sampler path; N = 64 (config 4 depth, beyond the
+    reference's MAX_DEPTH) runs through the same stream layout."""
+    from types import SimpleNamespace
+    rng = np.random.default_rng(3)
+    inputs = bp.MarketInputs(S0=50.0, K=52.0, q=0.03, sigma=0.4, T=1.0, N=14)
+    params = bp.with_custom_probs(inputs, rng.uniform(0.2, 0.8, size=14))
+    for tag in ("asian-call", "float-lookback", "lookback-put"):
+        req = bp.ValuationRequest(inputs=inputs, params=params, kind=bp.resolve_kind(tag))
+        draws = [700, 3, 5000, 1]
+        theta, sse, _ = bp.mc._strata_stats(req, 2, draws, 99, 0, 1)
+        ot, os_ = oracle.mc_strata(14, 50.0, 52.0, params.u, params.d, params.up_probs, tag, 2, draws, 99, 0, 1)
+        np.testing.assert_allclose(theta, ot, rtol=1e-12, atol=1e-12)
+        np.testing.assert_allclose(sse, os_, rtol=1e-9, atol=1e-9)
+    req64 = classic_req(64)
+    P = req64.params
+    theta, sse, _ = bp.mc._strata_stats(req64, 3, [2000] * 8, 5, 1, 1)
+    ot, os_ = oracle.mc_strata(64, 100.0, 100.0, P.u, P.d, P.up_probs, "asian-call", 3, [2000] * 8, 5, 1, 1)
+    np.testing.assert_allclose(theta, ot, rtol=1e-12)
+    np.testing.assert_allclose(sse, os_, rtol=1e-9)
+
+
+def test_sigma_zero_all_up_paths():
+    """p == 1 exactly (sigma = 0, model.py:128-132): every draw is the all-up path."""
+    inputs = bp.MarketInputs(S0=2.0, K=1.0, q=0.05, sigma=0.0, T=1.0, N=8)
+    params = bp.derive_crr(inputs)
+    req = bp.ValuationRequest(inputs=inputs, params=params, kind=bp.PayoffKind.EUROPEAN_CALL)
+    est = bp.estimate_basic(req, bp.McConfig(R=64, seed=1))
+    assert est.variance == 0.0
+    assert est.value == pytest.approx(math.exp(-0.05) * (2.0 * params.u ** 8 - 1.0), rel=1e-13)
