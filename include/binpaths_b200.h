@@ -71,6 +71,10 @@ enum bp_status {
 #define BP_FLAG_COUNT       1u  /* leaf bookkeeping: per-up-count histogram */
 #define BP_FLAG_GENERIC     2u  /* force the per-path walk kernel           */
 #define BP_FLAG_NO_TIMING   4u  /* skip the CUDA-event timing of the launch */
+#define BP_FLAG_THRESHOLD   8u  /* threshold-search engine: per node, binary
+                                   search of the class-sorted inner tables;
+                                   leaves are NOT visited one by one, report
+                                   its rate as "effective paths/s"          */
 
 /* One tree + contract.  Mirrors the fields the reference engine reads:
  * inputs.{S0,K,N} and params.{u,d,up_probs} (exact.py:87-99), with the
@@ -93,7 +97,7 @@ typedef struct bp_exact_result {
     uint64_t code_sum;            /* sum of visited path codes (mod 2^64)     */
     uint64_t hist[64];            /* BP_FLAG_COUNT: leaves per up-count h     */
     double   kernel_ms;           /* device time of the valuation (events)    */
-    int32_t  engine;              /* 0 = per-path walk, 1 = affine-threshold  */
+    int32_t  engine;              /* 0 path walk, 1 leaf tests, 2 search      */
     int32_t  inner_bits;          /* L, leaves per inner block = 2^L          */
     int32_t  n_superblocks;       /* canonical partial count                  */
     int32_t  n_devices;

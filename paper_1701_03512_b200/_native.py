@@ -22,6 +22,7 @@ N_PAYOFFS = 6
 FLAG_COUNT = 1
 FLAG_GENERIC = 2
 FLAG_NO_TIMING = 4
+FLAG_THRESHOLD = 8
 
 _STATUS = {
     1: E.InvalidInput,

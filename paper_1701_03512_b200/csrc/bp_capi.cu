@@ -19,6 +19,7 @@
 #include "../../include/binpaths_b200.h"
 #include "bp_exact.cuh"
 #include "bp_kernels.h"
+#include "bp_threshold.h"
 
 using namespace bp;
 
@@ -130,6 +131,23 @@ static void build_inner(int L, double u, double d, std::vector<double>& c, std::
 static Layout choose_layout(const bp_tree* t, uint32_t payoffs, uint32_t flags, bool* fast_possible) {
   const int N = t->n_steps;
   Layout lay{};
+  if ((flags & BP_FLAG_THRESHOLD) && N >= kFastMinN && constant_p(t) && t->up_probs[0] > 0.0 &&
+      t->up_probs[0] < 1.0 && t->u > t->d) {
+    // K8 threshold search: 2^LT leaves per node, >= 2^16 nodes when N allows
+    lay.engine = 2;
+    lay.L = std::max(8, std::min(20, N - 16));
+    lay.D = N - lay.L;
+    lay.m = 0;
+    lay.Dp = lay.D;
+    const int free_bits = lay.D - 5;
+    lay.q = std::max(0, free_bits - 18);
+    lay.units = 1ull << (free_bits - lay.q);
+    lay.g = 0;
+    lay.n_sb = (int)std::min<unsigned long long>(kMaxSB, lay.units);
+    lay.units_per_sb = lay.units / lay.n_sb;
+    if (fast_possible) *fast_possible = false;
+    return lay;
+  }
   bool fast = !(flags & BP_FLAG_GENERIC) && N >= kFastMinN && constant_p(t);
   if (fast) {
     const double p = t->up_probs[0];
@@ -344,6 +362,11 @@ struct bp_exact_plan {
   };
   std::vector<Group> groups;
   GenericArgs gen{};
+  // K8 tables (host copies; uploaded per device on first use)
+  std::vector<double> th_tables;  // [slot][val 2^LT | pre 2^LT + LT + 1]
+  int th_nt = 0;
+  ThresholdArgs th{};
+  double* th_dev[64] = {nullptr};
   struct Scratch {
     double2* p = nullptr;
     size_t bytes = 0;
@@ -368,6 +391,70 @@ static int plan_build(const bp_tree* t, uint32_t payoffs, uint32_t flags, bp_exa
       if (rc) return rc;
       P->groups.push_back(std::move(g));
     }
+  } else if (lay.engine == 2) {
+    const int LT = lay.L, NL = 1 << LT;
+    std::vector<double> c, mx, mn, e;
+    std::vector<int> h;
+    build_inner(LT, t->u, t->d, c, mx, mn, e, h);
+    ThresholdArgs& a = P->th;
+    // classes in popcount order: offsets, and the per-leaf position
+    std::vector<int> off(LT + 2, 0);
+    for (int cl = 0; cl <= LT; ++cl) off[cl + 1] = off[cl] + binom(LT, cl);
+    for (int cl = 0; cl <= LT + 1; ++cl) a.class_off[cl] = off[cl];
+    const size_t slot_sz = (size_t)NL + NL + LT + 1;
+    // kind slots in kind-bit order (k_exact_threshold walks k = 0..5)
+    std::vector<int> kinds;
+    for (int k = 0; k < kNumKinds; ++k)
+      if (((payoffs >> k) & 1) && k != kEC && k != kEP) kinds.push_back(k);
+    P->th_nt = (int)kinds.size();
+    P->th_tables.assign(slot_sz * std::max(1, P->th_nt), 0.0);
+    std::vector<std::vector<double>> cls(LT + 1);
+    for (int slot = 0; slot < P->th_nt; ++slot) {
+      const int k = kinds[slot];
+      const std::vector<double>& v = (k == kAC || k == kAP) ? c : (k == kFL) ? mx : mn;
+      const bool desc = (k == kAC || k == kFL);
+      for (auto& x : cls) x.clear();
+      for (int s2 = 0; s2 < NL; ++s2) cls[__builtin_popcount((unsigned)s2)].push_back(v[s2]);
+      double* val = P->th_tables.data() + slot * slot_sz;
+      double* pre = val + NL;
+      for (int cl = 0; cl <= LT; ++cl) {
+        auto& x = cls[cl];
+        if (desc)
+          std::sort(x.begin(), x.end(), [](double p1, double p2) { return p1 > p2; });
+        else
+          std::sort(x.begin(), x.end());
+        double sum = 0.0, comp = 0.0;
+        pre[off[cl] + cl] = 0.0;
+        for (size_t i = 0; i < x.size(); ++i) {
+          val[off[cl] + i] = x[i];
+          comp_add(sum, comp, x[i]);
+          pre[off[cl] + cl + i + 1] = sum + comp;
+        }
+      }
+    }
+    const int N = t->n_steps;
+    const double p = t->up_probs[0];
+    for (int k = 0; k < kMaxN + 2 + kMaxThreshL + 1; ++k)
+      a.w[k] = (k <= N) ? t->disc * std::pow(p, k) * std::pow(1.0 - p, N - k) : 0.0;
+    for (int cc = 0; cc <= LT; ++cc) {
+      double r = 1.0;
+      for (int j = 0; j < cc; ++j) r *= t->u;
+      for (int j = cc; j < LT; ++j) r *= t->d;
+      a.e_cls[cc] = r;
+      a.b_cls[cc] = (double)binom(LT, cc);
+    }
+    a.S0 = t->S0;
+    a.K = t->K;
+    a.NK = (double)N * t->K;
+    a.u = t->u;
+    a.d = t->d;
+    a.N = N;
+    a.LT = LT;
+    a.D = lay.D;
+    a.m = 0;
+    a.Dp = lay.D;
+    a.q = lay.q;
+    a.kinds = payoffs;
   } else {
     GenericArgs& g = P->gen;
     g.S0 = t->S0;
@@ -421,7 +508,30 @@ static int plan_enqueue(bp_exact_plan* P, int dev, int sb_first, int sb_count, d
   BP_CUDA(cudaMemsetAsync(out_dev, 0, sizeof(double) * 2 * kNumKinds * sb_count, st));
   const int sms = device_sm_count(dev);
   const unsigned long long want = (n_units + 7) / 8;
-  if (lay.engine == 1) {
+  if (lay.engine == 2) {
+    if (cnt) return fail(BP_E_INVALID_INPUT, "the threshold engine does not visit leaves (no bookkeeping)");
+    ThresholdArgs a = P->th;
+    {
+      std::lock_guard<std::mutex> g(P->mu);
+      if (!P->th_dev[dev] && !P->th_tables.empty()) {
+        BP_CUDA(cudaMalloc((void**)&P->th_dev[dev], sizeof(double) * P->th_tables.size()));
+        BP_CUDA(cudaMemcpyAsync(P->th_dev[dev], P->th_tables.data(), sizeof(double) * P->th_tables.size(),
+                                cudaMemcpyHostToDevice, st));
+      }
+    }
+    const size_t NL = (size_t)1 << lay.L, slot_sz = NL + NL + lay.L + 1;
+    for (int slot = 0; slot < P->th_nt; ++slot) {
+      a.val[slot] = P->th_dev[dev] + slot * slot_sz;
+      a.pre[slot] = a.val[slot] + NL;
+    }
+    a.unit_first = u0;
+    a.unit_end = u1;
+    const int occ = std::max(1, occupancy_exact_threshold());
+    const int grid = (int)std::max<unsigned long long>(1, std::min<unsigned long long>(want, (unsigned long long)occ * sms));
+    BP_CUDA(launch_exact_threshold(a, grid, st, unit_base));
+    BP_CUDA(launch_sb_reduce(unit_base, lay.units_per_sb, sb_first, sb_count, P->payoffs, 1.0 / P->tree.n_steps,
+                             out_dev, st));
+  } else if (lay.engine == 1) {
     bool first_group = true;  // bookkeeping once per valuation, not per kind group
     for (auto& g : P->groups) {
       const bool cnt_g = cnt && first_group;
@@ -447,6 +557,16 @@ static int plan_enqueue(bp_exact_plan* P, int dev, int sb_first, int sb_count, d
 
 static void plan_release_scratch(bp_exact_plan* P, cudaStream_t st) {
   for (int d = 0; d < 64; ++d)
+    if (P->th_dev[d]) {
+      int cur = 0;
+      cudaGetDevice(&cur);
+      cudaSetDevice(d);
+      cudaDeviceSynchronize();
+      cudaFree(P->th_dev[d]);
+      cudaSetDevice(cur);
+      P->th_dev[d] = nullptr;
+    }
+  for (int d = 0; d < 64; ++d)
     if (P->scratch[d].p) {
       int cur = 0;
       cudaGetDevice(&cur);
@@ -467,6 +587,11 @@ static int enqueue_superblocks(const bp_tree* t, uint32_t payoffs, uint32_t flag
   rc = plan_enqueue(&P, dev, sb_first, sb_count, out_dev, hist_dev, st);
   if (P.scratch[dev].p) cudaFreeAsync(P.scratch[dev].p, st);  // stream-ordered: after the kernels
   P.scratch[dev].p = nullptr;
+  if (P.th_dev[dev]) {  // K8 tables: the synchronous path frees them after the stream drains
+    cudaStreamSynchronize(st);
+    cudaFree(P.th_dev[dev]);
+    P.th_dev[dev] = nullptr;
+  }
   return rc;
 }
 
@@ -598,13 +723,26 @@ static void run_device_job(const bp_tree* t, uint32_t payoffs, uint32_t flags, D
   job->partials.assign(np, 0.0);
   job->hist.assign(66, 0ull);
   if (cnt) cudaMemsetAsync(c.hist_dev, 0, sizeof(unsigned long long) * 66, c.st);
+  keep_pool(job->device);
+  // host preparation (tables) happens before the timed window
+  bp_exact_plan P;
+  int rc = plan_build(t, payoffs, flags, &P);
+  if (!rc && P.lay.engine == 2 && !P.th_tables.empty()) {
+    // K8 tables: upload before the timed window as well
+    if ((e = cudaMalloc((void**)&P.th_dev[job->device], sizeof(double) * P.th_tables.size())) == cudaSuccess)
+      e = cudaMemcpyAsync(P.th_dev[job->device], P.th_tables.data(), sizeof(double) * P.th_tables.size(),
+                          cudaMemcpyHostToDevice, c.st);
+    if (e != cudaSuccess) return cuda_fail(e, "threshold tables");
+  }
   cudaEventRecord(c.e0, c.st);
-  int rc = enqueue_superblocks(t, payoffs, flags, job->device, job->sb_first, job->sb_count, c.out_dev,
-                               cnt ? c.hist_dev : nullptr, c.st);
+  if (!rc) rc = plan_enqueue(&P, job->device, job->sb_first, job->sb_count, c.out_dev, cnt ? c.hist_dev : nullptr, c.st);
+  if (P.scratch[job->device].p) cudaFreeAsync(P.scratch[job->device].p, c.st);
+  P.scratch[job->device].p = nullptr;
   if (rc) {
     job->rc = rc;
     job->err = g_err;
     cudaStreamSynchronize(c.st);
+    plan_release_scratch(&P, c.st);
     return;
   }
   cudaEventRecord(c.e1, c.st);
@@ -614,6 +752,7 @@ static void run_device_job(const bp_tree* t, uint32_t payoffs, uint32_t flags, D
   std::memcpy(job->partials.data(), c.out_host, sizeof(double) * np);
   if (cnt) std::memcpy(job->hist.data(), c.hist_host, sizeof(unsigned long long) * 66);
   cudaEventElapsedTime(&job->ms, c.e0, c.e1);
+  plan_release_scratch(&P, c.st);
 }
 
 extern "C" int bp_exact(const bp_tree* tree, uint32_t payoffs, uint32_t flags, int n_dev, const int* devices,
@@ -663,7 +802,7 @@ extern "C" int bp_exact(const bp_tree* tree, uint32_t payoffs, uint32_t flags, i
   bp_combine_superblocks(all.data(), lay.n_sb, payoffs, out->value);
   if (!(flags & BP_FLAG_COUNT)) out->leaves = 1ull << tree->n_steps;
   out->kernel_ms = ms;
-  out->engine = lay.engine;
+  out->engine = lay.engine;  // 0 path walk, 1 explicit leaf tests, 2 threshold search
   out->inner_bits = lay.L;
   out->n_superblocks = lay.n_sb;
   out->n_devices = G;

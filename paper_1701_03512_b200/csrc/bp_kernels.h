@@ -52,4 +52,10 @@ unsigned long long mc_chunk();
 
 cudaError_t launch_dfma_peak(double* out, int grid, int iters, cudaStream_t st);
 
+// K8 threshold-search engine, see bp_threshold_kernels.cu
+constexpr int kMaxThreshL = 22;
+struct ThresholdArgs;
+cudaError_t launch_exact_threshold(const ThresholdArgs& a, int grid, cudaStream_t st, double2* unit_out);
+int occupancy_exact_threshold();
+
 }  // namespace bp

@@ -102,12 +102,18 @@ def tree_of(req):
     return _native.make_tree(N, S0, float(inp.K), float(par.u), float(par.d), disc, probs)
 
 
+ENGINES = {0: "path-walk", 1: "affine-threshold", 2: "threshold-search"}
+
+
 def value_exact(req, kinds: Optional[Sequence] = None, devices: Optional[Sequence[int]] = None,
-                count: bool = False, generic: bool = False) -> ExactResult:
+                count: bool = False, generic: bool = False, search: bool = False) -> ExactResult:
     """Exact values of one or more payoff kinds in ONE pass over the 2^N paths.
 
     ``kinds`` defaults to ``[req.kind]``; ``count=True`` also returns the
-    leaf bookkeeping (paths per up count, code checksum).
+    leaf bookkeeping (paths per up count, code checksum).  ``search=True``
+    selects the threshold-search engine (K8): same exact value, but a node's
+    inner leaves are counted by binary search instead of being visited, so
+    its rate is an EFFECTIVE paths/s (not comparable to leaf evaluation).
     """
     _check_enumerable(req)
     kinds = [req.kind] if kinds is None else list(kinds)
@@ -118,14 +124,15 @@ def value_exact(req, kinds: Optional[Sequence] = None, devices: Optional[Sequenc
     devs = list(devices) if devices is not None else _devices(req)
     arr = (ctypes.c_int * len(devs))(*devs)
     res = _native.BpExactResult()
-    flags = (_native.FLAG_COUNT if count else 0) | (_native.FLAG_GENERIC if generic else 0)
+    flags = ((_native.FLAG_COUNT if count else 0) | (_native.FLAG_GENERIC if generic else 0)
+             | (_native.FLAG_THRESHOLD if search else 0))
     L = _native.lib()
     _native.check(L.bp_exact(ctypes.byref(tree), mask, flags, len(devs), arr, ctypes.byref(res)))
     del keep
     vals = {BIT_TAG[b]: float(res.value[b]) for b in range(_native.N_PAYOFFS) if (mask >> b) & 1}
     hist = np.array(res.hist[: req.inputs.N + 1], dtype=np.uint64) if count else None
     return ExactResult(values=vals, leaves=int(res.leaves), code_sum=int(res.code_sum), hist=hist,
-                       kernel_ms=float(res.kernel_ms), engine=("affine-threshold" if res.engine else "path-walk"),
+                       kernel_ms=float(res.kernel_ms), engine=ENGINES[int(res.engine)],
                        inner_bits=int(res.inner_bits), n_superblocks=int(res.n_superblocks),
                        n_devices=int(res.n_devices))
 

@@ -182,3 +182,35 @@ def test_config3_golden_N36_when_available():
     req = _req(36, 100.0, 105.0, 0.03, 2.0, g["u"], g["d"], g["p"])
     res = bp.value_exact(req, kinds=[bp.ASIAN_CALL])
     assert _close(res.values["asian-call"], g["asian_call"]), (res.values, g["asian_call"])
+
+
+@pytest.mark.parametrize("N", [16, 20, 24, 30])
+def test_threshold_search_engine_matches_leaf_engine(N):
+    """K8 (binary search over class-sorted tables) gives the
+    same exact value as the explicit leaf engine K1 and the oracle."""
+    rng = np.random.default_rng(100 + N)
+    S0 = float(rng.uniform(50, 150)); K = float(S0 * rng.uniform(0.85, 1.15))
+    r = float(rng.uniform(0.0, 0.08)); sigma = float(rng.uniform(0.1, 0.5)); T = float(rng.uniform(0.25, 3))
+    P = bp.classic_crr(N, sigma, r, T)
+    req = _req(N, S0, K, r, T, P.u, P.d, P.up_probs[0])
+    kinds = [bp.resolve_kind(k) for k in ALL]
+    a = bp.value_exact(req, kinds=kinds)
+    b = bp.value_exact(req, kinds=kinds, search=True)
+    assert b.engine == "threshold-search"
+    for k in ALL:
+        assert _close(b.values[k], a.values[k]), (N, k, a.values[k], b.values[k])
+
+
+def test_threshold_search_config_goldens():
+    g1 = load_golden("exact_config2.json")
+    req = _req(30, 100.0, g1["K"], 0.05, 1.0, g1["u"], g1["d"], g1["p"])
+    res = bp.value_exact(req, kinds=[bp.ASIAN_CALL, bp.FLOATING_LOOKBACK], search=True)
+    assert _close(res.values["asian-call"], g1["asian_call"])
+    assert _close(res.values["float-lookback"], g1["float_lookback"])
+    g = load_golden("exact_paper.json")
+    inputs = bp.MarketInputs(S0=g["S0"], K=g["K"], q=g["q"], sigma=g["sigma"], T=g["T"], N=32)
+    req = bp.ValuationRequest(inputs=inputs, params=bp.derive_crr(inputs), kind=bp.PayoffKind.ASIAN_PUT,
+                              force_large=True)
+    res = bp.value_exact(req, kinds=[bp.PayoffKind.ASIAN_PUT, bp.PayoffKind.FIXED_LOOKBACK_PUT], search=True)
+    for tag in ("asian-put", "lookback-put"):
+        assert _close(res.values[tag], g["values"][tag]), (tag, res.values[tag], g["values"][tag])
