@@ -50,13 +50,9 @@ constexpr int kMidMax = 64;          // 2^m, m <= 6
 constexpr int kUnitTargetLog2 = 14;  // units >= 2^14 when the tree allows it (r1 scan)
 constexpr int kMaxSB = 8;            // canonical super-blocks (top 3 bits)
 constexpr int kFastMinN = 16;        // smaller trees use the per-path walk
-constexpr unsigned kMaskHi = 0x01000000u;  // mask double 2^(16-1023)
-constexpr int kMaskExp = 1007;             // acc * 2^(1007 - a) = true sum
 
 struct ExactScalars {
   double S0, K, NK, u, d, invN;
-  double sc_up[3];   // 2^a_t : table t scale (thresholds are scaled alike)
-  double sc_dn[3];   // 2^(1007 - a_t) : unscale of the masked sums
   int N, L, D, m, Dp, n_mid;
   int q;             // a unit is 2^q consecutive 32-lane prefix groups
   int zero;          // opaque 0 (defeats constant hoisting in the leaf loop)
