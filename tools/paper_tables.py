@@ -1,0 +1,65 @@
+"""Reproduce the paper's Monte Carlo tables (Tables 3-5, N = 32,
+beta-CRR desk: S0=20, K=100, q=6%, sigma=3, T=1) on the GPU engine and print
+them beside the published values.  Mean over `reps` repetitions of the
+per-repetition estimates (the paper reports single runs / study averages).
+Table 4 ("R = 2^10", strata M = 1..64) is reproduced by proportional
+allocation (estimate_partitioned, mc.py:234-257), Table 5 by R draws per
+stratum (estimate_partitioned_equal) and the shared-sample estimator.
+"""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1701_03512_b200 as bp  # noqa: E402
+
+PUBLISHED = {
+    "table3_basic_var_asian": {512: 0.735, 1024: 0.362, 2048: 0.179, 4096: 0.095, 8192: 0.050, 16384: 0.022,
+                               32768: 0.011, 65536: 0.006},
+    "table3_basic_var_lookback": {512: 0.022, 1024: 0.009, 2048: 0.005, 4096: 0.002, 8192: 0.001},
+    "table4_partitioned_prop_var_asian": {1: 0.367, 2: 0.332, 4: 0.315, 8: 0.272, 16: 0.263, 32: 0.212, 64: 0.194},
+    "table4_partitioned_prop_var_lookback": {1: 0.010, 2: 0.009, 4: 0.008, 8: 0.008, 16: 0.008, 32: 0.007,
+                                             64: 0.007},
+    "table5_partitioned_var_asian": {1: 0.367, 2: 0.220, 4: 0.062, 8: 0.027, 16: 0.005, 32: 0.005, 64: 0.002},
+    "table5_shared_var_asian": {1: 0.373, 2: 0.305, 4: 0.267, 8: 0.203, 16: 0.170, 32: 0.142, 64: 0.123},
+}
+
+
+def desk(kind, N=32):
+    inputs = bp.MarketInputs(S0=20.0, K=100.0, q=0.06, sigma=3.0, T=1.0, N=N)
+    return bp.ValuationRequest(inputs=inputs, params=bp.derive_crr(inputs), kind=kind)
+
+
+def study(reps=200, seed=2017):
+    asian, look = desk(bp.PayoffKind.ASIAN_PUT), desk(bp.PayoffKind.FIXED_LOOKBACK_PUT)
+    out = {}
+    out["table3_basic_var_asian"] = {R: bp.run_repetitions(bp.estimate_basic, asian, bp.McConfig(R=R, seed=seed,
+                                     reps=reps)).mean_variance for R in PUBLISHED["table3_basic_var_asian"]}
+    out["table3_basic_var_lookback"] = {R: bp.run_repetitions(bp.estimate_basic, look, bp.McConfig(
+        R=R, seed=seed, reps=reps)).mean_variance for R in PUBLISHED["table3_basic_var_lookback"]}
+    for tag, req in (("asian", asian), ("lookback", look)):
+        out[f"table4_partitioned_prop_var_{tag}"] = {
+            M: bp.run_repetitions(bp.estimate_partitioned, req,
+                                  bp.McConfig(R=1024, M=M, seed=seed, reps=reps)).mean_variance
+            for M in PUBLISHED["table4_partitioned_prop_var_asian"]}
+    out["table5_partitioned_var_asian"] = {
+        M: bp.run_repetitions(bp.estimate_partitioned_equal, asian,
+                              bp.McConfig(R=1024, M=M, seed=seed, reps=reps)).mean_variance
+        for M in PUBLISHED["table5_partitioned_var_asian"]}
+    out["table5_shared_var_asian"] = {
+        M: bp.run_repetitions(bp.estimate_shared, asian,
+                              bp.McConfig(R=1024, M=M, seed=seed, reps=reps)).mean_variance
+        for M in PUBLISHED["table5_shared_var_asian"]}
+    return out
+
+
+if __name__ == "__main__":
+    reps = int(sys.argv[1]) if len(sys.argv) > 1 else 200
+    res = study(reps)
+    for name, pub in PUBLISHED.items():
+        print(name)
+        for k, v in pub.items():
+            ours = res[name][k]
+            print(f"  {k:>6}: published {v:8.3f}   gpu mean-of-estimates {ours:8.4f}   ratio {ours / v:6.3f}")
+    json.dump({"published": PUBLISHED, "gpu": res, "reps": reps}, open("gpurun_out/paper_tables.json", "w"),
+              indent=1)
