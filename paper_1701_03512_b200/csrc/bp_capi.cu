@@ -20,6 +20,7 @@
 #include "bp_exact.cuh"
 #include "bp_kernels.h"
 #include "bp_threshold.h"
+#include "bp_exact_w.cuh"
 
 using namespace bp;
 
@@ -146,6 +147,28 @@ static Layout choose_layout(const bp_tree* t, uint32_t payoffs, uint32_t flags, 
     lay.n_sb = (int)std::min<unsigned long long>(kMaxSB, lay.units);
     lay.units_per_sb = lay.units / lay.n_sb;
     if (fast_possible) *fast_possible = false;
+    return lay;
+  }
+  static const bool force_w = [] {
+    const char* e = std::getenv("BINPATHS_WEIGHTED");
+    return e && std::atoi(e) != 0;
+  }();
+  // K1w: per-leaf weights (any per-step probabilities) -- the explicit engine
+  // for non-constant p, and for constant p when BINPATHS_WEIGHTED=1
+  if (!(flags & BP_FLAG_GENERIC) && N >= kFastMinN && t->u > t->d && (force_w || !constant_p(t))) {
+    lay.engine = 3;
+    lay.L = 8;
+    lay.D = N - lay.L;
+    const int free_bits = lay.D - 5;
+    lay.m = std::max(2, std::min(6, free_bits - kUnitTargetLog2));  // >= 2: nodes go in fours
+    lay.Dp = lay.D - lay.m;
+    const int unit_bits = std::max(0, free_bits - lay.m);
+    lay.q = std::max(0, unit_bits - 18);
+    lay.units = 1ull << (unit_bits - lay.q);
+    lay.g = 0;
+    lay.n_sb = (int)std::min<unsigned long long>(kMaxSB, lay.units);
+    lay.units_per_sb = lay.units / lay.n_sb;
+    if (fast_possible) *fast_possible = true;
     return lay;
   }
   bool fast = !(flags & BP_FLAG_GENERIC) && N >= kFastMinN && constant_p(t);
@@ -295,12 +318,104 @@ static int fill_fast_args(const bp_tree* t, const Layout& lay, unsigned km, std:
   return BP_OK;
 }
 
+// K1w arguments: per-step weights, one sorted table per kind + group prefix sums
+static int fill_w_args(const bp_tree* t, const Layout& lay, unsigned km, std::vector<unsigned char>& buf) {
+  constexpr int L = 8, NL = 1 << L, NG = NL / 8;
+  buf.assign(sizeof(ExactWArgs<L>), 0);
+  ExactWArgs<L>& a = *reinterpret_cast<ExactWArgs<L>*>(buf.data());
+  const int N = t->n_steps, D = lay.D, m = lay.m, Dp = lay.Dp;
+  std::vector<double> c, mx, mn, e;
+  std::vector<int> h;
+  build_inner(L, t->u, t->d, c, mx, mn, e, h);
+  // inner weights: steps D .. N-1 (0-based), step D = most significant bit of s
+  std::vector<double> w(NL, 1.0);
+  for (int s2 = 0; s2 < NL; ++s2)
+    for (int j = 0; j < L; ++j) {
+      const double p = t->up_probs[D + j];
+      w[s2] *= ((s2 >> (L - 1 - j)) & 1) ? p : 1.0 - p;
+    }
+  std::vector<int> kinds;
+  for (int k = 0; k < kNumKinds; ++k)  // slot order = kind-bit order (k_exact_w)
+    if ((km >> k) & 1) kinds.push_back(k);
+  if (kinds.size() > 2) return fail(BP_E_INVALID_INPUT, "more than two kinds in one launch");
+  for (size_t slot = 0; slot < kinds.size(); ++slot) {
+    const int k = kinds[slot];
+    const std::vector<double>& v = (k == kAC || k == kAP) ? c : (k == kFL) ? mx : (k == kFLP) ? mn : e;
+    const bool desc = (k == kAC || k == kFL || k == kEC);
+    std::vector<int> ord(NL);
+    for (int i = 0; i < NL; ++i) ord[i] = i;
+    std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return desc ? v[x] > v[y] : v[x] < v[y]; });
+    for (int i = 0; i < NL; ++i) a.tab[slot * NL + i] = v[ord[i]];
+    for (int g = 0; g < NG; ++g) {
+      double sa = 0.0, ca = 0.0, sb = 0.0, cb = 0.0;
+      a.gp[slot][g * 9] = make_double2(0.0, 0.0);
+      for (int n = 1; n <= 8; ++n) {
+        const int s2 = ord[8 * g + n - 1];
+        comp_add(sa, ca, w[s2] * v[s2]);
+        comp_add(sb, cb, w[s2]);
+        a.gp[slot][g * 9 + n] = make_double2(sa + ca, sb + cb);
+      }
+    }
+  }
+  double E = 0.0, Ec = 0.0, O = 0.0, Oc = 0.0;
+  for (int s2 = 0; s2 < NL; ++s2) {
+    comp_add(E, Ec, w[s2] * e[s2]);
+    comp_add(O, Oc, w[s2]);
+  }
+  // middle tables (steps Dp .. D-1)
+  for (int j = 0; j < (1 << m); ++j) {
+    double r = 1.0, cs = 0.0, m1 = 0.0, m2 = INFINITY, ww = 1.0;
+    for (int i = 0; i < m; ++i) {
+      const int b = (j >> (m - 1 - i)) & 1;
+      const double p = t->up_probs[Dp + i];
+      r *= b ? t->u : t->d;
+      cs += r;
+      m1 = std::max(m1, r);
+      m2 = std::min(m2, r);
+      ww *= b ? p : 1.0 - p;
+    }
+    a.mid_c[j] = cs;
+    a.mid_e[j] = r;
+    a.mid_mx[j] = m1;
+    a.mid_mn[j] = m2;
+    a.mid_w[j] = ww;
+  }
+  for (int i = 0; i < Dp; ++i) {
+    a.p[i] = t->up_probs[i];
+    a.q[i] = 1.0 - t->up_probs[i];
+  }
+  ExactWScalars& sc = a.s;
+  sc.S0 = t->S0;
+  sc.K = t->K;
+  sc.NK = (double)N * t->K;
+  sc.u = t->u;
+  sc.d = t->d;
+  sc.disc = t->disc;
+  sc.E = E + Ec;
+  sc.Omega = O + Oc;
+  sc.N = N;
+  sc.L = L;
+  sc.D = D;
+  sc.m = m;
+  sc.Dp = Dp;
+  sc.n_mid = 1 << m;
+  sc.q = lay.q;
+  sc.zero = 0;
+  return BP_OK;
+}
+
 static int build_fast_args(const bp_tree* t, const Layout& lay, unsigned km, std::vector<unsigned char>& buf) {
   switch (lay.L) {
     case 8: return fill_fast_args<8>(t, lay, km, buf);
     case 9: return fill_fast_args<9>(t, lay, km, buf);
     default: return fail(BP_E_INVALID_INPUT, "unsupported inner block size");
   }
+}
+
+static void set_units_w(std::vector<unsigned char>& buf, unsigned long long u0, unsigned long long u1) {
+  ExactWScalars* s = &reinterpret_cast<ExactWArgs<8>*>(buf.data())->s;
+  s->unit_first = u0;
+  s->unit_end = u1;
 }
 
 static void set_units(std::vector<unsigned char>& buf, int L, unsigned long long u0, unsigned long long u1) {
@@ -383,7 +498,15 @@ static int plan_build(const bp_tree* t, uint32_t payoffs, uint32_t flags, bp_exa
   P->flags = flags;
   P->lay = choose_layout(t, payoffs, flags, nullptr);
   const Layout& lay = P->lay;
-  if (lay.engine == 1) {
+  if (lay.engine == 3) {
+    for (unsigned km : fast_groups(payoffs)) {
+      bp_exact_plan::Group g;
+      g.km = km;
+      int rc = fill_w_args(&P->tree, lay, km, g.args);
+      if (rc) return rc;
+      P->groups.push_back(std::move(g));
+    }
+  } else if (lay.engine == 1) {
     for (unsigned km : fast_groups(payoffs)) {
       bp_exact_plan::Group g;
       g.km = km;
@@ -508,7 +631,17 @@ static int plan_enqueue(bp_exact_plan* P, int dev, int sb_first, int sb_count, d
   BP_CUDA(cudaMemsetAsync(out_dev, 0, sizeof(double) * 2 * kNumKinds * sb_count, st));
   const int sms = device_sm_count(dev);
   const unsigned long long want = (n_units + 7) / 8;
-  if (lay.engine == 2) {
+  if (lay.engine == 3) {
+    if (cnt) return fail(BP_E_INVALID_INPUT, "leaf bookkeeping runs on the class engine (constant p)");
+    for (auto& g : P->groups) {
+      set_units_w(g.args, u0, u1);
+      const int occ = std::max(1, occupancy_exact_w(g.km));
+      const int grid = (int)std::max<unsigned long long>(1, std::min<unsigned long long>(want, (unsigned long long)occ * sms));
+      BP_CUDA(launch_exact_w(g.km, g.args.data(), grid, st, unit_base));
+      BP_CUDA(launch_sb_reduce(unit_base, lay.units_per_sb, sb_first, sb_count, g.km, 1.0 / P->tree.n_steps,
+                               out_dev, st));
+    }
+  } else if (lay.engine == 2) {
     if (cnt) return fail(BP_E_INVALID_INPUT, "the threshold engine does not visit leaves (no bookkeeping)");
     ThresholdArgs a = P->th;
     {

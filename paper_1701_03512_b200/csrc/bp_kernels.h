@@ -52,6 +52,10 @@ unsigned long long mc_chunk();
 
 cudaError_t launch_dfma_peak(double* out, int grid, int iters, cudaStream_t st);
 
+// K1w per-leaf-weight enumeration (any per-step probabilities), bp_exact_w_kernels.cu
+cudaError_t launch_exact_w(unsigned km, const void* args, int grid, cudaStream_t st, double2* unit_out);
+int occupancy_exact_w(unsigned km);
+
 // K8 threshold-search engine, see bp_threshold_kernels.cu
 constexpr int kMaxThreshL = 22;
 struct ThresholdArgs;

@@ -102,7 +102,7 @@ def tree_of(req):
     return _native.make_tree(N, S0, float(inp.K), float(par.u), float(par.d), disc, probs)
 
 
-ENGINES = {0: "path-walk", 1: "affine-threshold", 2: "threshold-search"}
+ENGINES = {0: "path-walk", 1: "affine-threshold", 2: "threshold-search", 3: "affine-threshold-weighted"}
 
 
 def value_exact(req, kinds: Optional[Sequence] = None, devices: Optional[Sequence[int]] = None,

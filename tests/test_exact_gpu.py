@@ -214,3 +214,21 @@ def test_threshold_search_config_goldens():
     res = bp.value_exact(req, kinds=[bp.PayoffKind.ASIAN_PUT, bp.PayoffKind.FIXED_LOOKBACK_PUT], search=True)
     for tag in ("asian-put", "lookback-put"):
         assert _close(res.values[tag], g["values"][tag]), (tag, res.values[tag], g["values"][tag])
+
+
+@pytest.mark.parametrize("N", [16, 19, 22])
+def test_per_step_probabilities_weighted_engine(N):
+    """with_custom_probs trees (model.py:152-161): the per-leaf-weight engine K1w
+    vs the oracle and the path-walk engine, every kind."""
+    rng = np.random.default_rng(7 + N)
+    inputs = bp.MarketInputs(S0=50.0, K=51.0, q=0.02, sigma=0.35, T=1.5, N=N)
+    params = bp.with_custom_probs(inputs, rng.uniform(0.25, 0.75, size=N))
+    req = bp.ValuationRequest(inputs=inputs, params=params, kind=bp.ASIAN_CALL, force_large=True)
+    kinds = [bp.resolve_kind(k) for k in ALL]
+    a = bp.value_exact(req, kinds=kinds)
+    assert a.engine == "affine-threshold-weighted"
+    b = bp.value_exact(req, kinds=kinds, generic=True)
+    want = oracle.exact(N, 50.0, 51.0, params.u, params.d, params.up_probs, math.exp(-0.02 * 1.5), ALL, workers=8)
+    for k in ALL:
+        assert _close(a.values[k], want[k]), (N, k, a.values[k], want[k])
+        assert _close(b.values[k], want[k]), (N, k, b.values[k], want[k])
