@@ -35,17 +35,52 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(p) <= t for p in deps())
 
 
+def fast_parts() -> int:
+    import re
+    with open(os.path.join(HERE, "csrc", "bp_kernels.h")) as f:
+        return int(re.search(r"kFastParts = (\d+)", f.read()).group(1))
+
+
+def units():
+    """(source, extra nvcc flags, object) per translation unit; the K1
+    instantiation file is compiled once per part."""
+    out = []
+    for src in sources():
+        base = os.path.join(HERE, "_lib", "obj", os.path.basename(src)[:-3])
+        if src.endswith("bp_exact_fast_inst.cu"):
+            out += [(src, [f"-DBP_FAST_PART={i}"], f"{base}_{i}.o") for i in range(fast_parts())]
+        else:
+            out.append((src, [], base + ".o"))
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
+    """One nvcc per translation unit, in parallel (the template-heavy kernel
+    files dominate), then one host link with static cudart."""
     if not force and up_to_date():
         return OUT
-    os.makedirs(os.path.dirname(OUT), exist_ok=True)
+    os.makedirs(os.path.join(HERE, "_lib", "obj"), exist_ok=True)
     nvcc = os.environ.get("NVCC", "nvcc")
+    compile_flags = [f for f in FLAGS if f != "-shared"]
+    from concurrent.futures import ThreadPoolExecutor
+
+    def run(u):
+        src, extra, obj = u
+        cmd = [nvcc, *ARCH, *compile_flags, *extra, "-c", "-o", obj, src]
+        if verbose:
+            cmd.insert(1, "-Xptxas=-v")
+            print(" ".join(cmd), flush=True)
+        return subprocess.call(cmd)
+
+    todo = units()
+    with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
+        rcs = list(ex.map(run, todo))
+    failed = [u[0] + " " + " ".join(u[1]) for u, rc in zip(todo, rcs) if rc != 0]
+    if failed:
+        raise subprocess.CalledProcessError(1, f"nvcc {failed}")
     tmp = OUT + ".tmp"
-    cmd = [nvcc, *ARCH, *FLAGS, "-o", tmp, *sources()]
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd), flush=True)
-    subprocess.check_call(cmd)
+    subprocess.check_call([nvcc, *ARCH, "-shared", "-cudart", "static", "-Xcompiler", "-fPIC",
+                           "-o", tmp, *[u[2] for u in todo]])
     os.replace(tmp, OUT)
     return OUT
 

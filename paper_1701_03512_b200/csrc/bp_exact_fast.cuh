@@ -1,0 +1,236 @@
+// K1 k_exact_fast: the affine-threshold class walk (see bp_exact.cuh).
+// Kept in a header so build.py can compile one (L, kind-mask) instantiation
+// per translation unit (bp_exact_fast_inst.cu) in parallel.
+#pragma once
+#include <cmath>
+#include "bp_exact.cuh"
+#include "bp_kernels.h"
+#include "bp_leaf.cuh"
+
+#ifndef BP_TAB_SMEM
+#define BP_TAB_SMEM 0  // inner tables: 0 = constant bank (uniform LDCU), 1 = shared memory (LDS.128)
+#endif
+
+namespace bp {
+
+
+// resident CTAs per SM the register allocation targets: 3 for one table
+// (<= 85 registers), 2 for the fused two-table kernels (measured best, r1)
+__host__ __device__ constexpr int fast_tables(unsigned km) {
+  return (int)((km >> kAC) & 1) + (int)((km >> kAP) & 1) + (int)((km >> kFL) & 1) + (int)((km >> kFLP) & 1);
+}
+template <int L, unsigned KM, bool CNT>
+__global__ void __launch_bounds__(256, fast_tables(KM) == 2 ? 2 : 3)
+k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_out,
+             unsigned long long* __restrict__ hist) {
+  constexpr int NC = L + 1;
+  constexpr int NG = n_groups(L);
+  constexpr bool kAC_ = (KM >> kAC) & 1, kAP_ = (KM >> kAP) & 1, kFL_ = (KM >> kFL) & 1,
+                 kFLP_ = (KM >> kFLP) & 1, kEC_ = (KM >> kEC) & 1, kEP_ = (KM >> kEP) & 1;
+  constexpr bool needMx = kFL_, needMn = kFLP_;
+  // table slots in kind order AC, AP, FL, FLP
+  constexpr int NT = (int)kAC_ + (int)kAP_ + (int)kFL_ + (int)kFLP_;
+  static_assert(NT <= 2, "at most two tables per launch");
+  constexpr int slotAC = 0, slotAP = (int)kAC_, slotFL = (int)kAC_ + (int)kAP_, slotFLP = slotFL + (int)kFL_;
+  // nodes per leaf block: each table load feeds NP compares
+  constexpr int NP = 2;
+
+  __shared__ double sw[kMaxN + 2 + NC];
+  __shared__ unsigned long long shist[kMaxN + 2];
+  __shared__ double sgpre[NT > 0 ? NT : 1][NG * kGroupSlots];
+#if BP_TAB_SMEM
+  __shared__ __align__(16) double stab[NT > 0 ? NT << L : 2];
+  for (int i = threadIdx.x; i < (NT << L); i += blockDim.x) stab[i] = a.tab[i];
+#endif
+  for (int i = threadIdx.x; i < kMaxN + 2 + NC; i += blockDim.x) sw[i] = (i < kMaxN + 2) ? a.w[i] : 0.0;
+  for (int t = 0; t < NT; ++t)
+    for (int i = threadIdx.x; i < NG * kGroupSlots; i += blockDim.x) sgpre[t][i] = (&a.gpre[t][0][0])[i];
+  if (CNT)
+    for (int i = threadIdx.x; i < kMaxN + 2; i += blockDim.x) shist[i] = 0ull;
+  __syncthreads();
+
+  const ExactScalars& sc = a.s;
+  const int lane = threadIdx.x & 31;
+  const unsigned long long warp_global = (blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x) >> 5;
+  const unsigned long long n_warps = (gridDim.x * (unsigned long long)blockDim.x) >> 5;
+  const double INF = __longlong_as_double(0x7ff0000000000000ll);
+  unsigned long long leaves = 0, code_sum = 0;
+
+  for (unsigned long long unit = sc.unit_first + warp_global; unit < sc.unit_end; unit += n_warps) {
+    double ts[kNumKinds], tc[kNumKinds];
+#pragma unroll
+    for (int k = 0; k < kNumKinds; ++k) { ts[k] = 0.0; tc[k] = 0.0; }
+   for (unsigned long long rr = 0; rr < (1ull << sc.q); ++rr) {
+    const unsigned long long tp = (((unit << sc.q) | rr) << 5) | (unsigned long long)lane;  // thread prefix, Dp bits
+    // --- prefix walk: steps 1..Dp (reference asset_path, model.py:164-172)
+    double S = sc.S0, Sig = 0.0, Mx = 0.0, Mn = INF;
+    int h = 0;
+    for (int t = sc.Dp - 1; t >= 0; --t) {
+      const int b = (int)((tp >> t) & 1ull);
+      S *= b ? sc.u : sc.d;
+      Sig += S;
+      if (needMx) Mx = fmax(Mx, S);
+      if (needMn) Mn = fmin(Mn, S);
+      h += b;
+    }
+
+    // nodes are processed NP at a time (n_mid is a multiple of NP: m >= 1)
+    for (int j0 = 0; j0 < sc.n_mid; j0 += NP) {
+      double Sn[NP], Sg[NP], Mxn[NP], Mnn[NP], base[NP], thC[NP], thX[NP], thN[NP];
+      int hn[NP];
+#pragma unroll
+      for (int p = 0; p < NP; ++p) {
+        // --- node state at depth D
+        const int j = j0 + p;
+        Sn[p] = S * a.mid_e[j];
+        Sg[p] = fma(S, a.mid_c[j], Sig);
+        Mxn[p] = needMx ? fmax(Mx, S * a.mid_mx[j]) : 0.0;
+        Mnn[p] = needMn ? fmin(Mn, S * a.mid_mn[j]) : 0.0;
+        hn[p] = h + a.mid_h[j];
+        base[p] = Sg[p] - sc.NK;
+        const double rS = 1.0 / Sn[p];
+        thC[p] = (kAC_ || kAP_) ? -base[p] * rS : 0.0;
+        thX[p] = kFL_ ? Mxn[p] * rS : 0.0;
+        thN[p] = kFLP_ ? fmin(Mnn[p], sc.K) * rS : 0.0;
+      }
+
+#if BP_TAB_SMEM
+      const double2* tb = reinterpret_cast<const double2*>(stab) + (j0 & sc.zero);  // + 0, opaque
+#else
+      const double2* tb = reinterpret_cast<const double2*>(a.tab) + (j0 & sc.zero);  // + 0, opaque
+#endif
+      // --- per kind: the leaf block (2^L explicit leaf tests per node), then
+      // the class finalisation, node value = sum_c w[h+c] * contrib_c.  Kinds
+      // run one after the other so only one kind's accumulators are live.
+      if (kAC_) {
+        double acc[NP][NC];
+        int cnt[NP][NC];
+        zero_acc<NP, NC>(acc, cnt);
+        leaf_block<L, NP, slotAC, true>(tb, sgpre[slotAC], thC, acc, cnt);
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          double v = 0.0;
+#pragma unroll
+          for (int c = 0; c < NC; ++c) v = fma(sw[hn[p] + c], fma(Sn[p], acc[p][c], base[p] * (double)cnt[p][c]), v);
+          comp_add(ts[kAC], tc[kAC], v);
+        }
+      }
+      if (kAP_) {
+        double acc[NP][NC];
+        int cnt[NP][NC];
+        zero_acc<NP, NC>(acc, cnt);
+        leaf_block<L, NP, slotAP, false>(tb, sgpre[slotAP], thC, acc, cnt);
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          double v = 0.0;
+#pragma unroll
+          for (int c = 0; c < NC; ++c) v = fma(sw[hn[p] + c], fma(-Sn[p], acc[p][c], -base[p] * (double)cnt[p][c]), v);
+          comp_add(ts[kAP], tc[kAP], v);
+        }
+      }
+      if (kFL_) {
+        double acc[NP][NC];
+        int cnt[NP][NC];
+        zero_acc<NP, NC>(acc, cnt);
+        leaf_block<L, NP, slotFL, true>(tb, sgpre[slotFL], thX, acc, cnt);
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          double v = 0.0;
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            // S A + Mx (C_c - n) - S e_c C_c
+            const double bc = a.b_cls[c];
+            const double t = fma(Sn[p], acc[p][c], Mxn[p] * (bc - (double)cnt[p][c]));
+            v = fma(sw[hn[p] + c], fma(-Sn[p] * a.e_cls[c], bc, t), v);
+          }
+          comp_add(ts[kFL], tc[kFL], v);
+        }
+      }
+      if (kFLP_) {
+        double acc[NP][NC];
+        int cnt[NP][NC];
+        zero_acc<NP, NC>(acc, cnt);
+        leaf_block<L, NP, slotFLP, false>(tb, sgpre[slotFLP], thN, acc, cnt);
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          double v = 0.0;
+          const double flat = fmax(sc.K - Mnn[p], 0.0);
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            const double n = (double)cnt[p][c];
+            const double t = fma(sc.K, n, -Sn[p] * acc[p][c]);
+            v = fma(sw[hn[p] + c], fma(a.b_cls[c] - n, flat, t), v);
+          }
+          comp_add(ts[kFLP], tc[kFLP], v);
+        }
+      }
+      if (kEC_ || kEP_) {
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          double vEC = 0.0, vEP = 0.0;
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            const double wv = sw[hn[p] + c], bc = a.b_cls[c];
+            if (kEC_) vEC = fma(wv, bc * fmax(fma(Sn[p], a.e_cls[c], -sc.K), 0.0), vEC);
+            if (kEP_) vEP = fma(wv, bc * fmax(fma(-Sn[p], a.e_cls[c], sc.K), 0.0), vEP);
+          }
+          if (kEC_) comp_add(ts[kEC], tc[kEC], vEC);
+          if (kEP_) comp_add(ts[kEP], tc[kEP], vEP);
+        }
+      }
+
+      if (CNT) {
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          // leaf bookkeeping (K6): leaves per total up count, code coverage
+          const unsigned long long node = (tp << sc.m) | (unsigned long long)(j0 + p);
+#pragma unroll
+          for (int c = 0; c < NC; ++c) atomicAdd(&shist[hn[p] + c], (unsigned long long)binom(L, c));
+          leaves += 1ull << L;
+          // sum of codes node*2^L + s, s < 2^L
+          code_sum += (node << (2 * L)) + (((1ull << L) * ((1ull << L) - 1)) >> 1);
+        }
+      }
+    }
+   }  // rr
+    // --- per-unit partial: fixed warp tree, lane 0 stores
+#pragma unroll
+    for (int k = 0; k < kNumKinds; ++k) {
+      if (!((KM >> k) & 1)) continue;
+      double s = ts[k], c = tc[k];
+      warp_comp_reduce(s, c);
+      if (lane == 0) unit_out[unit * kNumKinds + k] = make_double2(s, c);
+    }
+  }
+  if (CNT) {
+    atomicAdd(&hist[64], leaves);
+    atomicAdd(&hist[65], code_sum);
+    __syncthreads();
+    for (int i = threadIdx.x; i < kMaxN + 1; i += blockDim.x)
+      if (shist[i]) atomicAdd(&hist[i], shist[i]);
+  }
+}
+
+// launch wrappers
+template <int L, unsigned KM>
+cudaError_t launch_fast_t(const void* args, bool cnt, int grid, cudaStream_t st, double2* unit_out,
+                                 unsigned long long* hist) {
+  const ExactArgs<L>& a = *static_cast<const ExactArgs<L>*>(args);
+  if (cnt)
+    k_exact_fast<L, KM, true><<<grid, 256, 0, st>>>(a, unit_out, hist);
+  else
+    k_exact_fast<L, KM, false><<<grid, 256, 0, st>>>(a, unit_out, hist);
+  return cudaGetLastError();
+}
+
+template <int L, unsigned KM>
+int occupancy_fast_t(bool cnt) {
+  int n = 0;
+  if (cnt)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_exact_fast<L, KM, true>, 256, 0);
+  else
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_exact_fast<L, KM, false>, 256, 0);
+  return n;
+}
+
+}  // namespace bp

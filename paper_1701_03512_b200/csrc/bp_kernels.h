@@ -62,4 +62,11 @@ struct ThresholdArgs;
 cudaError_t launch_exact_threshold(const ThresholdArgs& a, int grid, cudaStream_t st, double2* unit_out);
 int occupancy_exact_threshold();
 
+// the K1 (L, kind mask) instantiations: every single kind plus the fused
+// config-2 pair (Asian call + floating lookback)
+#define BP_FAST_KMS(X, L)                                                      \
+  X(L, (1u << kAC)) X(L, (1u << kAP)) X(L, (1u << kFL)) X(L, (1u << kFLP))     \
+  X(L, (1u << kEC)) X(L, (1u << kEP)) X(L, ((1u << kAC) | (1u << kFL)))
+constexpr int kFastParts = 14;  // BP_FAST_KMS x L in {8, 9}: parts of bp_exact_fast_inst.cu
+
 }  // namespace bp
