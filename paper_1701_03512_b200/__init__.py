@@ -22,4 +22,6 @@ from .mc import (Estimate, McConfig, PhiloxStream, RepetitionSummary, allocate_s
 from .exact import (LARGE_DEPTH, ExactResult, ValuationRequest, price_batch, value_exact, value_exact_batch,
                     value_exact_parallel, value_exact_serial, value_leaf_formula)
 
+from .bench import BENCH_CSV_HEADER, BenchRecord, records_to_csv, records_to_tables, run_bench
+
 __version__ = "0.1.0"

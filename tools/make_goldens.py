@@ -20,6 +20,7 @@ Usage:
   python tools/make_goldens.py batch            # ~30 s on 8 cores
   python tools/make_goldens.py mc               # ~2 min
   python tools/make_goldens.py config3          # ~90 min on 8 cores
+  python tools/make_goldens.py cli              # seconds
 """
 
 from __future__ import annotations
@@ -355,11 +356,49 @@ def gen_mc():
     dump("mc_reference.json", out)
 
 
+def gen_cli():
+    """Reference CLI / bench-harness outputs: report values of the exact
+    methods and the bench CSV / table rendering of fixed records."""
+    from binpaths import cli
+    from binpaths.bench import BenchRecord, records_to_csv, records_to_tables
+    import contextlib
+    import io
+
+    def run(*argv):
+        buf = io.StringIO()
+        with contextlib.redirect_stdout(buf):
+            code = cli.main(list(argv))
+        return code, buf.getvalue()
+
+    desk = ["--S0", "20", "--K", "100", "--q", "0.06", "--sigma", "3.0", "--T", "1"]
+    price = []
+    for method in ("exact", "exact-serial", "leaf"):
+        for payoff in ("euro-call", "euro-put", "asian-put", "lookback-put"):
+            if method == "leaf" and payoff in ("asian-put", "lookback-put"):
+                continue
+            for N, workers in ((12, 1), (12, 4), (16, 3)):
+                argv = ["price", "--method", method, "--payoff", payoff, "--N", str(N), "--workers", str(workers)]
+                code, out = run(*argv, *desk)
+                rep = json.loads(out)
+                rep.pop("wall_seconds")
+                price.append({"argv": argv + desk, "code": code, "report": rep})
+    code, out = run("price", "--method", "exact", "--payoff", "euro-put", "--S0", "4", "--K", "5", "--q", "0",
+                    "--sigma", "0.30", "--T", "1", "--N", "2", "--override-u", "2", "--override-p", "0.5")
+    hand = json.loads(out)
+    hand.pop("wall_seconds")
+    recs = [BenchRecord(n=n, m=m, wall_seconds=w, speedup=s, efficiency=s / m, baseline_m=b)
+            for n, m, w, s, b in ((8, 1, 0.5, 1.0, 1), (8, 2, 0.26, 1.0 / 0.52, 1), (8, 4, 0.1301, 0.5 / 0.1301, 1),
+                                  (10, 2, 1.25, 2.0, 2), (10, 4, 0.7, 2.5 / 0.7, 2))]
+    fmt = {"records": [r.__dict__ for r in recs], "csv": records_to_csv(recs), "tables": records_to_tables(recs)}
+    dump("cli_reference.json", {"provenance": provenance(), "price": price, "hand_example": hand, "bench_format": fmt})
+
+
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
     which = sys.argv[1:] or ["small"]
     table = {"small": gen_small, "config1": gen_config1, "config2": gen_config2,
-             "config3": gen_config3, "paper": gen_paper, "batch": gen_batch, "mc": gen_mc}
+             "config3": gen_config3, "paper": gen_paper, "batch": gen_batch, "mc": gen_mc,
+             "cli": gen_cli}
     for w in which:
         t = time.time()
         table[w]()
