@@ -72,7 +72,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
             print(" ".join(cmd), flush=True)
         return subprocess.call(cmd)
 
-    todo = units()
+    # incremental: an object is rebuilt when its source or any header is newer
+    headers = [d for d in deps() if not d.endswith(".cu")]
+    newest_header = max(os.path.getmtime(h) for h in headers)
+    all_units = units()
+    todo = [u for u in all_units if force or not os.path.exists(u[2]) or
+            os.path.getmtime(u[2]) < max(newest_header, os.path.getmtime(u[0]))]
     with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
         rcs = list(ex.map(run, todo))
     failed = [u[0] + " " + " ".join(u[1]) for u, rc in zip(todo, rcs) if rc != 0]
@@ -80,9 +85,37 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise subprocess.CalledProcessError(1, f"nvcc {failed}")
     tmp = OUT + ".tmp"
     subprocess.check_call([nvcc, *ARCH, "-shared", "-cudart", "static", "-Xcompiler", "-fPIC",
-                           "-o", tmp, *[u[2] for u in todo]])
+                           "-o", tmp, *[u[2] for u in all_units]])
     os.replace(tmp, OUT)
     return OUT
+
+
+def build_variant(name: str, defines, parts=None, all_units: bool = False) -> str:
+    """Diagnostics: the library with extra -D flags on the K1 instantiation
+    parts (all parts, or the listed ones; every unit with all_units=True)
+    -> _lib/variants/<name>.so, for
+    BINPATHS_LIB=... scans (tools/scan_variants.sh).  Other objects are
+    shared with the main build."""
+    build()
+    nvcc = os.environ.get("NVCC", "nvcc")
+    compile_flags = [f for f in FLAGS if f != "-shared"]
+    vdir = os.path.join(HERE, "_lib", "variants", name)
+    os.makedirs(vdir, exist_ok=True)
+    objs, procs = [], []
+    for src, extra, obj in units():
+        part = next((int(e.split("=")[1]) for e in extra if e.startswith("-DBP_FAST_PART=")), None)
+        if not all_units and (part is None or (parts is not None and part not in parts)):
+            objs.append(obj)
+            continue
+        vobj = os.path.join(vdir, os.path.basename(obj))
+        objs.append(vobj)
+        procs.append(subprocess.Popen([nvcc, *ARCH, *compile_flags, *extra, *[f"-D{d}" for d in defines],
+                                       "-c", "-o", vobj, src]))
+    if any(p.wait() != 0 for p in procs):
+        raise subprocess.CalledProcessError(1, f"variant {name}")
+    out = os.path.join(HERE, "_lib", "variants", name + ".so")
+    subprocess.check_call([nvcc, *ARCH, "-shared", "-cudart", "static", "-Xcompiler", "-fPIC", "-o", out, *objs])
+    return out
 
 
 if __name__ == "__main__":

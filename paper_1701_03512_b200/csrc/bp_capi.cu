@@ -7,10 +7,12 @@
 // mc.py:92-100,197-213,287-331 (Monte Carlo).
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <list>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -404,12 +406,55 @@ static int fill_w_args(const bp_tree* t, const Layout& lay, unsigned km, std::ve
   return BP_OK;
 }
 
+// K1 arguments depend on the contract (S0, K) only through three scalars;
+// the tables (class-sorted inner tables, group prefix sums, middle tables,
+// weights) are a function of the lattice.  A small LRU of built argument
+// blocks keyed by the lattice makes revaluing on a known lattice (new spot or
+// strike, or the same contract again) skip the host table build (~20 us).
+struct FastArgsKey {
+  int L, D, m, Dp, q, N;
+  unsigned km;
+  double u, d, p, disc;
+  bool operator==(const FastArgsKey& o) const {
+    return L == o.L && D == o.D && m == o.m && Dp == o.Dp && q == o.q && N == o.N && km == o.km && u == o.u &&
+           d == o.d && p == o.p && disc == o.disc;
+  }
+};
+
+static void set_contract(std::vector<unsigned char>& buf, int L, const bp_tree* t) {
+  ExactScalars* s = (L == 8) ? &reinterpret_cast<ExactArgs<8>*>(buf.data())->s
+                             : &reinterpret_cast<ExactArgs<9>*>(buf.data())->s;
+  s->S0 = t->S0;
+  s->K = t->K;
+  s->NK = (double)t->n_steps * t->K;
+}
+
 static int build_fast_args(const bp_tree* t, const Layout& lay, unsigned km, std::vector<unsigned char>& buf) {
+  static std::mutex mu;
+  static std::list<std::pair<FastArgsKey, std::vector<unsigned char>>> lru;  // most recent first
+  constexpr size_t kCap = 16;
+  const FastArgsKey key{lay.L, lay.D, lay.m, lay.Dp, lay.q, t->n_steps, km, t->u, t->d, t->up_probs[0], t->disc};
+  {
+    std::lock_guard<std::mutex> g(mu);
+    for (auto it = lru.begin(); it != lru.end(); ++it)
+      if (it->first == key) {
+        lru.splice(lru.begin(), lru, it);
+        buf = it->second;
+        set_contract(buf, lay.L, t);
+        return BP_OK;
+      }
+  }
+  int rc;
   switch (lay.L) {
-    case 8: return fill_fast_args<8>(t, lay, km, buf);
-    case 9: return fill_fast_args<9>(t, lay, km, buf);
+    case 8: rc = fill_fast_args<8>(t, lay, km, buf); break;
+    case 9: rc = fill_fast_args<9>(t, lay, km, buf); break;
     default: return fail(BP_E_INVALID_INPUT, "unsupported inner block size");
   }
+  if (rc) return rc;
+  std::lock_guard<std::mutex> g(mu);
+  lru.emplace_front(key, buf);
+  if (lru.size() > kCap) lru.pop_back();
+  return BP_OK;
 }
 
 static void set_units_w(std::vector<unsigned char>& buf, unsigned long long u0, unsigned long long u1) {
@@ -454,9 +499,26 @@ static void keep_pool(int dev) {
   done[dev] = true;
 }
 
+// occupancy of a K1 instantiation (a property of the compiled kernel and the
+// device type; queried once)
+static int cached_occupancy_fast(int L, unsigned km, bool cnt) {
+  static std::mutex mu;
+  static std::vector<std::pair<unsigned, int>> memo;
+  const unsigned key = ((unsigned)L << 16) | (km << 1) | (cnt ? 1u : 0u);
+  std::lock_guard<std::mutex> g(mu);
+  for (auto& e : memo)
+    if (e.first == key) return e.second;
+  const int occ = occupancy_exact_fast(L, km, cnt);
+  memo.emplace_back(key, occ);
+  return occ;
+}
+
 static int device_sm_count(int dev) {
+  static std::atomic<int> memo[64];
+  if (dev >= 0 && dev < 64 && memo[dev].load() > 0) return memo[dev].load();
   int n = 0;
   cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  if (n > 0 && dev >= 0 && dev < 64) memo[dev].store(n);
   return n > 0 ? n : 1;
 }
 
@@ -670,7 +732,7 @@ static int plan_enqueue(bp_exact_plan* P, int dev, int sb_first, int sb_count, d
       const bool cnt_g = cnt && first_group;
       first_group = false;
       set_units(g.args, lay.L, u0, u1);
-      const int occ = std::max(1, occupancy_exact_fast(lay.L, g.km, cnt_g));
+      const int occ = std::max(1, cached_occupancy_fast(lay.L, g.km, cnt_g));
       const int grid = (int)std::max<unsigned long long>(1, std::min<unsigned long long>(want, (unsigned long long)occ * sms));
       BP_CUDA(launch_exact_fast(lay.L, g.km, g.args.data(), cnt_g, grid, st, unit_base, hist_dev));
       BP_CUDA(launch_sb_reduce(unit_base, lay.units_per_sb, sb_first, sb_count, g.km, 1.0 / P->tree.n_steps,
@@ -822,6 +884,8 @@ struct DevCtx {
   unsigned long long* hist_dev = nullptr;  // 66
   double* out_host = nullptr;              // pinned
   unsigned long long* hist_host = nullptr; // pinned
+  double2* scratch = nullptr;              // unit partials, grown on demand, kept
+  size_t scratch_bytes = 0;
 };
 static DevCtx g_ctx[64];
 
@@ -858,8 +922,15 @@ static void run_device_job(const bp_tree* t, uint32_t payoffs, uint32_t flags, D
   if (cnt) cudaMemsetAsync(c.hist_dev, 0, sizeof(unsigned long long) * 66, c.st);
   keep_pool(job->device);
   // host preparation (tables) happens before the timed window
+  static const bool trace = [] {
+    const char* e = std::getenv("BINPATHS_TRACE");
+    return e && std::atoi(e) != 0;
+  }();
+  using clk = std::chrono::steady_clock;
+  const auto t0 = clk::now();
   bp_exact_plan P;
   int rc = plan_build(t, payoffs, flags, &P);
+  const auto t1 = clk::now();
   if (!rc && P.lay.engine == 2 && !P.th_tables.empty()) {
     // K8 tables: upload before the timed window as well
     if ((e = cudaMalloc((void**)&P.th_dev[job->device], sizeof(double) * P.th_tables.size())) == cudaSuccess)
@@ -868,9 +939,13 @@ static void run_device_job(const bp_tree* t, uint32_t payoffs, uint32_t flags, D
     if (e != cudaSuccess) return cuda_fail(e, "threshold tables");
   }
   cudaEventRecord(c.e0, c.st);
+  P.scratch[job->device].p = c.scratch;  // the context's buffer (plan_enqueue grows it if needed)
+  P.scratch[job->device].bytes = c.scratch_bytes;
   if (!rc) rc = plan_enqueue(&P, job->device, job->sb_first, job->sb_count, c.out_dev, cnt ? c.hist_dev : nullptr, c.st);
-  if (P.scratch[job->device].p) cudaFreeAsync(P.scratch[job->device].p, c.st);
+  c.scratch = P.scratch[job->device].p;
+  c.scratch_bytes = P.scratch[job->device].bytes;
   P.scratch[job->device].p = nullptr;
+  P.scratch[job->device].bytes = 0;
   if (rc) {
     job->rc = rc;
     job->err = g_err;
@@ -881,7 +956,16 @@ static void run_device_job(const bp_tree* t, uint32_t payoffs, uint32_t flags, D
   cudaEventRecord(c.e1, c.st);
   cudaMemcpyAsync(c.out_host, c.out_dev, sizeof(double) * np, cudaMemcpyDeviceToHost, c.st);
   if (cnt) cudaMemcpyAsync(c.hist_host, c.hist_dev, sizeof(unsigned long long) * 66, cudaMemcpyDeviceToHost, c.st);
+  const auto t2 = clk::now();
   if ((e = cudaStreamSynchronize(c.st)) != cudaSuccess) return cuda_fail(e, "valuation");
+  if (trace) {
+    const auto t3 = clk::now();
+    auto us = [](clk::duration d) { return std::chrono::duration<double, std::micro>(d).count(); };
+    float kms = 0.f;
+    cudaEventElapsedTime(&kms, c.e0, c.e1);
+    std::fprintf(stderr, "[bp trace] dev %d: plan %.1f us, enqueue %.1f us, sync %.1f us, device %.1f us\n",
+                 job->device, us(t1 - t0), us(t2 - t1), us(t3 - t2), 1e3 * kms);
+  }
   std::memcpy(job->partials.data(), c.out_host, sizeof(double) * np);
   if (cnt) std::memcpy(job->hist.data(), c.hist_host, sizeof(unsigned long long) * 66);
   cudaEventElapsedTime(&job->ms, c.e0, c.e1);
