@@ -198,6 +198,36 @@ def time_workload(w, classic_crr, steps, warmup, rank, world, dev, group):
     return times, vals, sh, req, kinds
 
 
+def e2e_seconds(bp, req, kinds, args, warmup, rank, world, dev, group):
+    """Median wall seconds of one public-API valuation (host request in,
+    Python floats out), max over ranks.  N = 1: value_exact (C ABI, one
+    synchronous call); N > 1: value_exact_distributed on every rank (this
+    rank's super-blocks, the NCCL all_gather, the host combine)."""
+    import torch
+    import torch.distributed as dist
+    from paper_1701_03512_b200 import dist as bpd
+
+    ts = []
+    for i in range(warmup + args.steps):
+        if world > 1:
+            dist.barrier(group=group)
+        t0 = time.perf_counter()
+        if world == 1:
+            bp.value_exact(req, kinds=kinds, devices=[dev])
+        else:
+            bpd.value_exact_distributed(req, kinds, rank=rank, world=world, device=dev, group=group)
+        dt = time.perf_counter() - t0
+        if i >= warmup:
+            ts.append(dt)
+    med = statistics.median(ts)
+    if world > 1:
+        t = torch.tensor([med], dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+        med = float(t.item())
+        return med, "paper_1701_03512_b200.dist.value_exact_distributed(req, kinds, rank, world) on every rank"
+    return med, "paper_1701_03512_b200.value_exact(req, kinds) -> bp_exact (C ABI)"
+
+
 def kernel_share(w, classic_crr, dev, reps=5):
     """Duration of the dominant kernel alone (the leaf kernel + its reduce are
     what one super-block launch enqueues) for the roofline line."""
@@ -338,6 +368,10 @@ def run_ours(args):
     if rank == 0 and not args.no_config3:
         extra45 = secondary_configs(dev)
 
+    # e2e: the public API with host inputs and the result read back every step;
+    # for N > 1 every rank takes part (value_exact_distributed: its shard + NCCL)
+    e2e_s, e2e_path = e2e_seconds(bp, req, kinds, args, warmup, rank, world, dev, group)
+
     if rank != 0:
         if world > 1:
             dist.barrier()
@@ -364,19 +398,10 @@ def run_ours(args):
             "peak_kind": "measured DFMA microbenchmark (bp_fp64_peak, K7) on this GPU",
             "nominal_peak_Tops": 148 * 64 * 1.965e9 / 1e12}
 
-    # e2e: public API with host inputs, result read back, every step
-    e2e_times = []
-    for i in range(warmup + args.steps):
-        t0 = time.perf_counter()
-        r = bp.value_exact(req, kinds=kinds, devices=[dev])
-        dt = time.perf_counter() - t0
-        if i >= warmup:
-            e2e_times.append(dt)
-    e2e_s = statistics.median(e2e_times)
     h2d = 8 * w["N"] + 7 * 8 + 4  # the tree + per-step probabilities handed to the C ABI
     e2e = {"value": total_paths / e2e_s, "unit": "paths/s", "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": 8 * 6 * 2 * sh.n_sb, "seconds_per_step": e2e_s,
-           "path": "paper_1701_03512_b200.value_exact(req, kinds) -> bp_exact (C ABI)"}
+           "path": e2e_path}
 
     cpu = cpu_baseline(w, classic_crr) if world == 1 else None
     launches_per_step = 2 * (1 if set(w["kinds"]) == {"asian-call", "float-lookback"} else len(w["kinds"]))

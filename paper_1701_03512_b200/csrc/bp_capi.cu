@@ -16,6 +16,7 @@
 #include <mutex>
 #include <string>
 #include <thread>
+#include <utility>
 #include <vector>
 
 #include "../../include/binpaths_b200.h"
@@ -690,7 +691,9 @@ static int plan_enqueue(bp_exact_plan* P, int dev, int sb_first, int sb_count, d
   }
   // kernels index unit_out by absolute unit; shift the base pointer
   double2* unit_base = unit_out - (ptrdiff_t)(u0 * kNumKinds);
-  BP_CUDA(cudaMemsetAsync(out_dev, 0, sizeof(double) * 2 * kNumKinds * sb_count, st));
+  // no memset: the first K2 of the valuation also writes 0 for the kinds no
+  // launch group computes (zero_kinds)
+  unsigned zero_kinds = ~P->payoffs & ((1u << kNumKinds) - 1);
   const int sms = device_sm_count(dev);
   const unsigned long long want = (n_units + 7) / 8;
   if (lay.engine == 3) {
@@ -700,7 +703,7 @@ static int plan_enqueue(bp_exact_plan* P, int dev, int sb_first, int sb_count, d
       const int occ = std::max(1, occupancy_exact_w(g.km));
       const int grid = (int)std::max<unsigned long long>(1, std::min<unsigned long long>(want, (unsigned long long)occ * sms));
       BP_CUDA(launch_exact_w(g.km, g.args.data(), grid, st, unit_base));
-      BP_CUDA(launch_sb_reduce(unit_base, lay.units_per_sb, sb_first, sb_count, g.km, 1.0 / P->tree.n_steps,
+      BP_CUDA(launch_sb_reduce(unit_base, lay.units_per_sb, sb_first, sb_count, g.km, std::exchange(zero_kinds, 0u), 1.0 / P->tree.n_steps,
                                out_dev, st));
     }
   } else if (lay.engine == 2) {
@@ -724,7 +727,7 @@ static int plan_enqueue(bp_exact_plan* P, int dev, int sb_first, int sb_count, d
     const int occ = std::max(1, occupancy_exact_threshold());
     const int grid = (int)std::max<unsigned long long>(1, std::min<unsigned long long>(want, (unsigned long long)occ * sms));
     BP_CUDA(launch_exact_threshold(a, grid, st, unit_base));
-    BP_CUDA(launch_sb_reduce(unit_base, lay.units_per_sb, sb_first, sb_count, P->payoffs, 1.0 / P->tree.n_steps,
+    BP_CUDA(launch_sb_reduce(unit_base, lay.units_per_sb, sb_first, sb_count, P->payoffs, std::exchange(zero_kinds, 0u), 1.0 / P->tree.n_steps,
                              out_dev, st));
   } else if (lay.engine == 1) {
     bool first_group = true;  // bookkeeping once per valuation, not per kind group
@@ -735,7 +738,7 @@ static int plan_enqueue(bp_exact_plan* P, int dev, int sb_first, int sb_count, d
       const int occ = std::max(1, cached_occupancy_fast(lay.L, g.km, cnt_g));
       const int grid = (int)std::max<unsigned long long>(1, std::min<unsigned long long>(want, (unsigned long long)occ * sms));
       BP_CUDA(launch_exact_fast(lay.L, g.km, g.args.data(), cnt_g, grid, st, unit_base, hist_dev));
-      BP_CUDA(launch_sb_reduce(unit_base, lay.units_per_sb, sb_first, sb_count, g.km, 1.0 / P->tree.n_steps,
+      BP_CUDA(launch_sb_reduce(unit_base, lay.units_per_sb, sb_first, sb_count, g.km, std::exchange(zero_kinds, 0u), 1.0 / P->tree.n_steps,
                                out_dev, st));
     }
   } else {
@@ -745,7 +748,7 @@ static int plan_enqueue(bp_exact_plan* P, int dev, int sb_first, int sb_count, d
     const int occ = std::max(1, occupancy_exact_generic(cnt));
     const int grid = (int)std::max<unsigned long long>(1, std::min<unsigned long long>(want, (unsigned long long)occ * sms));
     BP_CUDA(launch_exact_generic(g, cnt, grid, st, unit_base, hist_dev));
-    BP_CUDA(launch_sb_reduce(unit_base, lay.units_per_sb, sb_first, sb_count, P->payoffs, 1.0, out_dev, st));
+    BP_CUDA(launch_sb_reduce(unit_base, lay.units_per_sb, sb_first, sb_count, P->payoffs, std::exchange(zero_kinds, 0u), 1.0, out_dev, st));
   }
   return BP_OK;
 }

@@ -79,11 +79,15 @@ k_exact_generic(const __grid_constant__ GenericArgs a, double2* __restrict__ uni
 // K2: super-block reduce.  Block b reduces the units of super-block
 // sb_first + b in a fixed order (thread-contiguous chunks, fixed tree), and
 // writes (sum, comp) per kind scaled by scale[k] (1/N for Asian kinds).
+// Kinds in zero_kinds (requested by no launch group of the valuation) are
+// written as 0, so every output entry is written exactly once per step.
 __global__ void __launch_bounds__(256)
 k_sb_reduce(const double2* __restrict__ unit_out, unsigned long long units_per_sb, int sb_first,
-            unsigned kinds, double scale_asian, double* __restrict__ out) {
+            unsigned kinds, unsigned zero_kinds, double scale_asian, double* __restrict__ out) {
   __shared__ double ss[256], sc2[256];
   const unsigned long long u0 = (unsigned long long)(sb_first + blockIdx.x) * units_per_sb;
+  if (threadIdx.x < 2 * kNumKinds && ((zero_kinds >> (threadIdx.x >> 1)) & 1))
+    out[blockIdx.x * kNumKinds * 2 + threadIdx.x] = 0.0;
   for (int k = 0; k < kNumKinds; ++k) {
     if (!((kinds >> k) & 1)) continue;
     double s = 0.0, c = 0.0;
@@ -182,8 +186,8 @@ int occupancy_exact_generic(bool cnt) {
 }
 
 cudaError_t launch_sb_reduce(const double2* unit_out, unsigned long long units_per_sb, int sb_first, int sb_count,
-                             unsigned kinds, double scale_asian, double* out, cudaStream_t st) {
-  k_sb_reduce<<<sb_count, 256, 0, st>>>(unit_out, units_per_sb, sb_first, kinds, scale_asian, out);
+                             unsigned kinds, unsigned zero_kinds, double scale_asian, double* out, cudaStream_t st) {
+  k_sb_reduce<<<sb_count, 256, 0, st>>>(unit_out, units_per_sb, sb_first, kinds, zero_kinds, scale_asian, out);
   return cudaGetLastError();
 }
 

@@ -19,7 +19,7 @@ cudaError_t launch_exact_generic(const GenericArgs& a, bool cnt, int grid, cudaS
 int occupancy_exact_generic(bool cnt);
 
 cudaError_t launch_sb_reduce(const double2* unit_out, unsigned long long units_per_sb, int sb_first, int sb_count,
-                             unsigned kinds, double scale_asian, double* out, cudaStream_t st);
+                             unsigned kinds, unsigned zero_kinds, double scale_asian, double* out, cudaStream_t st);
 
 // Batched exact (one option per CTA group), see bp_batch_kernels.cu
 struct BatchOption {
