@@ -35,6 +35,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 W_OPS = {"asian-call": 3, "float-lookback": 3}  # FP64-pipe ops per path per payoff
+# one metric string for both arms (ours and --impl reference)
+METRIC = "exact-enumeration paths/sec (N=30 two payoffs in one pass; N=36 under config3)"
 
 
 def workloads():
@@ -47,6 +49,12 @@ def workloads():
         "config2": dict(N=30, S0=100.0, K=K2, r=0.05, sigma=0.2, T=1.0, kinds=["asian-call", "float-lookback"]),
         "config3": dict(N=36, S0=100.0, K=105.0, r=0.03, sigma=0.3, T=2.0, kinds=["asian-call"]),
     }, classic_crr
+
+
+def workload_config(name, w):
+    """The workload keys both arms report (same config for the driver's ratio)."""
+    return {"workload": name, "N": w["N"], "payoffs": w["kinds"], "K": w["K"], "S0": w["S0"], "r": w["r"],
+            "sigma": w["sigma"], "T": w["T"]}
 
 
 def make_req(w, classic_crr):
@@ -148,11 +156,11 @@ def run_reference(args):
             steps.append(cb)
     v = statistics.median(s["value"] for s in steps)
     total = 1 << w["N"]
-    line = {"metric": f"exact-enumeration paths/sec ({args.workload}, N={w['N']})", "value": v, "unit": "paths/s",
+    line = {"metric": METRIC, "value": v, "unit": "paths/s",
             "n_gpus": 0, "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / v * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": args.workload, "N": w["N"], "payoffs": w["kinds"], "K": w["K"]},
+            "config": {**workload_config(args.workload, w), "parallelism": f"{os.cpu_count()} host threads"},
             "cpu_baseline": {**steps[-1], "value": v},
             "e2e": {"value": v, "unit": "paths/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -406,12 +414,11 @@ def run_ours(args):
     cpu = cpu_baseline(w, classic_crr) if world == 1 else None
     launches_per_step = 2 * (1 if set(w["kinds"]) == {"asian-call", "float-lookback"} else len(w["kinds"]))
     line = {
-        "metric": "exact-enumeration paths/sec (N=30 two payoffs in one pass; N=36 under config3)",
+        "metric": METRIC,
         "value": value, "unit": "paths/s", "n_gpus": world, "steps": args.steps, "warmup": warmup,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (BASELINE configs; tree parameters, no dataset)",
-        "config": {"workload": args.workload, "N": w["N"], "payoffs": w["kinds"], "K": w["K"], "S0": w["S0"],
-                   "r": w["r"], "sigma": w["sigma"], "T": w["T"], "parallelism": f"superblock-shard x{world}",
+        "config": {**workload_config(args.workload, w), "parallelism": f"superblock-shard x{world}",
                    "l2": "flushed (256 MiB write) between timed steps", "engine": "affine-threshold" if sh.engine else
                    "path-walk", "inner_bits": sh.inner_bits, "superblocks": sh.n_sb},
         "values": vals, "config3": extra or None, **extra45, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,

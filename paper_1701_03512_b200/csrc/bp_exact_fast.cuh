@@ -6,7 +6,6 @@
 #include "bp_exact.cuh"
 #include "bp_kernels.h"
 #include "bp_leaf.cuh"
-#include <type_traits>
 
 #ifndef BP_TAB_SMEM
 #define BP_TAB_SMEM 0  // inner tables: 0 = constant bank (uniform LDCU), 1 = shared memory (LDS.128)
@@ -20,14 +19,8 @@ namespace bp {
 __host__ __device__ constexpr int fast_tables(unsigned km) {
   return (int)((km >> kAC) & 1) + (int)((km >> kAP) & 1) + (int)((km >> kFL) & 1) + (int)((km >> kFLP) & 1);
 }
-#ifndef BP_FUSED_PASSES
-#define BP_FUSED_PASSES 0  // 0: all kinds in one node pass (measured best, r1 scan); 1: one pass per table kind
-#endif
-#ifndef BP_FUSED_MINB
-#define BP_FUSED_MINB(KM) (fast_tables(KM) == 2 ? 2 : 3)  // resident CTAs per SM (r1 scan)
-#endif
 template <int L, unsigned KM, bool CNT>
-__global__ void __launch_bounds__(256, BP_FUSED_MINB(KM))
+__global__ void __launch_bounds__(256, fast_tables(KM) == 2 ? 2 : 3)
 k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_out,
              unsigned long long* __restrict__ hist) {
   constexpr int NC = L + 1;
@@ -81,146 +74,124 @@ k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_
       h += b;
     }
 
-    // One pass over the thread's nodes per table kind (the prefix walk above
-    // is shared): only one kind's per-class accumulators and thresholds are
-    // live at a time, so the fused config-2 kernel fits the single-kind
-    // register budget.  The European kinds (no table) ride on the first pass.
-    auto node_pass = [&](auto pass_tag) {
-      constexpr unsigned PM = decltype(pass_tag)::value;
-      constexpr bool FIRST = (PM >> 31) & 1;
-      constexpr bool pAC = (PM >> kAC) & 1, pAP = (PM >> kAP) & 1, pFL = (PM >> kFL) & 1,
-                     pFLP = (PM >> kFLP) & 1, pEC = (PM >> kEC) & 1, pEP = (PM >> kEP) & 1;
-      // nodes are processed NP at a time (n_mid is a multiple of NP: m >= 1)
-      for (int j0 = 0; j0 < sc.n_mid; j0 += NP) {
-        double Sn[NP], Sg[NP], Mxn[NP], Mnn[NP], base[NP], thC[NP], thX[NP], thN[NP];
-        int hn[NP];
+    // nodes are processed NP at a time (n_mid is a multiple of NP: m >= 1)
+    for (int j0 = 0; j0 < sc.n_mid; j0 += NP) {
+      double Sn[NP], Sg[NP], Mxn[NP], Mnn[NP], base[NP], thC[NP], thX[NP], thN[NP];
+      int hn[NP];
 #pragma unroll
-        for (int p = 0; p < NP; ++p) {
-          // --- node state at depth D
-          const int j = j0 + p;
-          Sn[p] = S * a.mid_e[j];
-          Sg[p] = fma(S, a.mid_c[j], Sig);
-          Mxn[p] = pFL ? fmax(Mx, S * a.mid_mx[j]) : 0.0;
-          Mnn[p] = pFLP ? fmin(Mn, S * a.mid_mn[j]) : 0.0;
-          hn[p] = h + a.mid_h[j];
-          base[p] = Sg[p] - sc.NK;
-          const double rS = 1.0 / Sn[p];
-          thC[p] = (pAC || pAP) ? -base[p] * rS : 0.0;
-          thX[p] = pFL ? Mxn[p] * rS : 0.0;
-          thN[p] = pFLP ? fmin(Mnn[p], sc.K) * rS : 0.0;
-        }
+      for (int p = 0; p < NP; ++p) {
+        // --- node state at depth D
+        const int j = j0 + p;
+        Sn[p] = S * a.mid_e[j];
+        Sg[p] = fma(S, a.mid_c[j], Sig);
+        Mxn[p] = needMx ? fmax(Mx, S * a.mid_mx[j]) : 0.0;
+        Mnn[p] = needMn ? fmin(Mn, S * a.mid_mn[j]) : 0.0;
+        hn[p] = h + a.mid_h[j];
+        base[p] = Sg[p] - sc.NK;
+        const double rS = 1.0 / Sn[p];
+        thC[p] = (kAC_ || kAP_) ? -base[p] * rS : 0.0;
+        thX[p] = kFL_ ? Mxn[p] * rS : 0.0;
+        thN[p] = kFLP_ ? fmin(Mnn[p], sc.K) * rS : 0.0;
+      }
 
 #if BP_TAB_SMEM
-        const double2* tb = reinterpret_cast<const double2*>(stab) + (j0 & sc.zero);  // + 0, opaque
+      const double2* tb = reinterpret_cast<const double2*>(stab) + (j0 & sc.zero);  // + 0, opaque
 #else
-        const double2* tb = reinterpret_cast<const double2*>(a.tab) + (j0 & sc.zero);  // + 0, opaque
+      const double2* tb = reinterpret_cast<const double2*>(a.tab) + (j0 & sc.zero);  // + 0, opaque
 #endif
-        // --- per kind: the leaf block (2^L explicit leaf tests per node), then
-        // the class finalisation, node value = sum_c w[h+c] * contrib_c.  Kinds
-        // run one after the other so only one kind's accumulators are live.
-        if (pAC) {
-          double acc[NP][NC];
-          int cnt[NP][NC];
-          zero_acc<NP, NC>(acc, cnt);
-          leaf_block<L, NP, slotAC, true>(tb, sgpre[slotAC], thC, acc, cnt);
+      // --- per kind: the leaf block (2^L explicit leaf tests per node), then
+      // the class finalisation, node value = sum_c w[h+c] * contrib_c.  Kinds
+      // run one after the other so only one kind's accumulators are live.
+      if (kAC_) {
+        double acc[NP][NC];
+        int cnt[NP][NC];
+        zero_acc<NP, NC>(acc, cnt);
+        leaf_block<L, NP, slotAC, true>(tb, sgpre[slotAC], thC, acc, cnt);
 #pragma unroll
-          for (int p = 0; p < NP; ++p) {
-            double v = 0.0;
+        for (int p = 0; p < NP; ++p) {
+          double v = 0.0;
 #pragma unroll
-            for (int c = 0; c < NC; ++c) v = fma(sw[hn[p] + c], fma(Sn[p], acc[p][c], base[p] * (double)cnt[p][c]), v);
-            comp_add(ts[kAC], tc[kAC], v);
-          }
-        }
-        if (pAP) {
-          double acc[NP][NC];
-          int cnt[NP][NC];
-          zero_acc<NP, NC>(acc, cnt);
-          leaf_block<L, NP, slotAP, false>(tb, sgpre[slotAP], thC, acc, cnt);
-#pragma unroll
-          for (int p = 0; p < NP; ++p) {
-            double v = 0.0;
-#pragma unroll
-            for (int c = 0; c < NC; ++c) v = fma(sw[hn[p] + c], fma(-Sn[p], acc[p][c], -base[p] * (double)cnt[p][c]), v);
-            comp_add(ts[kAP], tc[kAP], v);
-          }
-        }
-        if (pFL) {
-          double acc[NP][NC];
-          int cnt[NP][NC];
-          zero_acc<NP, NC>(acc, cnt);
-          leaf_block<L, NP, slotFL, true>(tb, sgpre[slotFL], thX, acc, cnt);
-#pragma unroll
-          for (int p = 0; p < NP; ++p) {
-            double v = 0.0;
-#pragma unroll
-            for (int c = 0; c < NC; ++c) {
-              // S A + Mx (C_c - n) - S e_c C_c
-              const double bc = a.b_cls[c];
-              const double t = fma(Sn[p], acc[p][c], Mxn[p] * (bc - (double)cnt[p][c]));
-              v = fma(sw[hn[p] + c], fma(-Sn[p] * a.e_cls[c], bc, t), v);
-            }
-            comp_add(ts[kFL], tc[kFL], v);
-          }
-        }
-        if (pFLP) {
-          double acc[NP][NC];
-          int cnt[NP][NC];
-          zero_acc<NP, NC>(acc, cnt);
-          leaf_block<L, NP, slotFLP, false>(tb, sgpre[slotFLP], thN, acc, cnt);
-#pragma unroll
-          for (int p = 0; p < NP; ++p) {
-            double v = 0.0;
-            const double flat = fmax(sc.K - Mnn[p], 0.0);
-#pragma unroll
-            for (int c = 0; c < NC; ++c) {
-              const double n = (double)cnt[p][c];
-              const double t = fma(sc.K, n, -Sn[p] * acc[p][c]);
-              v = fma(sw[hn[p] + c], fma(a.b_cls[c] - n, flat, t), v);
-            }
-            comp_add(ts[kFLP], tc[kFLP], v);
-          }
-        }
-        if (pEC || pEP) {
-#pragma unroll
-          for (int p = 0; p < NP; ++p) {
-            double vEC = 0.0, vEP = 0.0;
-#pragma unroll
-            for (int c = 0; c < NC; ++c) {
-              const double wv = sw[hn[p] + c], bc = a.b_cls[c];
-              if (pEC) vEC = fma(wv, bc * fmax(fma(Sn[p], a.e_cls[c], -sc.K), 0.0), vEC);
-              if (pEP) vEP = fma(wv, bc * fmax(fma(-Sn[p], a.e_cls[c], sc.K), 0.0), vEP);
-            }
-            if (pEC) comp_add(ts[kEC], tc[kEC], vEC);
-            if (pEP) comp_add(ts[kEP], tc[kEP], vEP);
-          }
-        }
-
-        if (CNT && FIRST) {
-#pragma unroll
-          for (int p = 0; p < NP; ++p) {
-            // leaf bookkeeping (K6): leaves per total up count, code coverage
-            const unsigned long long node = (tp << sc.m) | (unsigned long long)(j0 + p);
-#pragma unroll
-            for (int c = 0; c < NC; ++c) atomicAdd(&shist[hn[p] + c], (unsigned long long)binom(L, c));
-            leaves += 1ull << L;
-            // sum of codes node*2^L + s, s < 2^L
-            code_sum += (node << (2 * L)) + (((1ull << L) * ((1ull << L) - 1)) >> 1);
-          }
+          for (int c = 0; c < NC; ++c) v = fma(sw[hn[p] + c], fma(Sn[p], acc[p][c], base[p] * (double)cnt[p][c]), v);
+          comp_add(ts[kAC], tc[kAC], v);
         }
       }
-    };
-    // pass masks: bit 31 marks the first pass (bookkeeping + European kinds)
-#if BP_FUSED_PASSES
-    constexpr unsigned kEu = KM & ((1u << kEC) | (1u << kEP));
-    constexpr unsigned kTabs[4] = {KM & (1u << kAC), KM & (1u << kAP), KM & (1u << kFL), KM & (1u << kFLP)};
-    constexpr int t0 = kTabs[0] ? 0 : kTabs[1] ? 1 : kTabs[2] ? 2 : kTabs[3] ? 3 : 4;
-    node_pass(std::integral_constant<unsigned, (1u << 31) | kEu | (t0 < 4 ? kTabs[t0 < 4 ? t0 : 0] : 0u)>{});
-    if constexpr (t0 < 1 && kTabs[1]) node_pass(std::integral_constant<unsigned, kTabs[1]>{});
-    if constexpr (t0 < 2 && kTabs[2]) node_pass(std::integral_constant<unsigned, kTabs[2]>{});
-    if constexpr (t0 < 3 && kTabs[3]) node_pass(std::integral_constant<unsigned, kTabs[3]>{});
-#else
-    node_pass(std::integral_constant<unsigned, (1u << 31) | KM>{});
-#endif
+      if (kAP_) {
+        double acc[NP][NC];
+        int cnt[NP][NC];
+        zero_acc<NP, NC>(acc, cnt);
+        leaf_block<L, NP, slotAP, false>(tb, sgpre[slotAP], thC, acc, cnt);
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          double v = 0.0;
+#pragma unroll
+          for (int c = 0; c < NC; ++c) v = fma(sw[hn[p] + c], fma(-Sn[p], acc[p][c], -base[p] * (double)cnt[p][c]), v);
+          comp_add(ts[kAP], tc[kAP], v);
+        }
+      }
+      if (kFL_) {
+        double acc[NP][NC];
+        int cnt[NP][NC];
+        zero_acc<NP, NC>(acc, cnt);
+        leaf_block<L, NP, slotFL, true>(tb, sgpre[slotFL], thX, acc, cnt);
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          double v = 0.0;
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            // S A + Mx (C_c - n) - S e_c C_c
+            const double bc = a.b_cls[c];
+            const double t = fma(Sn[p], acc[p][c], Mxn[p] * (bc - (double)cnt[p][c]));
+            v = fma(sw[hn[p] + c], fma(-Sn[p] * a.e_cls[c], bc, t), v);
+          }
+          comp_add(ts[kFL], tc[kFL], v);
+        }
+      }
+      if (kFLP_) {
+        double acc[NP][NC];
+        int cnt[NP][NC];
+        zero_acc<NP, NC>(acc, cnt);
+        leaf_block<L, NP, slotFLP, false>(tb, sgpre[slotFLP], thN, acc, cnt);
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          double v = 0.0;
+          const double flat = fmax(sc.K - Mnn[p], 0.0);
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            const double n = (double)cnt[p][c];
+            const double t = fma(sc.K, n, -Sn[p] * acc[p][c]);
+            v = fma(sw[hn[p] + c], fma(a.b_cls[c] - n, flat, t), v);
+          }
+          comp_add(ts[kFLP], tc[kFLP], v);
+        }
+      }
+      if (kEC_ || kEP_) {
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          double vEC = 0.0, vEP = 0.0;
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            const double wv = sw[hn[p] + c], bc = a.b_cls[c];
+            if (kEC_) vEC = fma(wv, bc * fmax(fma(Sn[p], a.e_cls[c], -sc.K), 0.0), vEC);
+            if (kEP_) vEP = fma(wv, bc * fmax(fma(-Sn[p], a.e_cls[c], sc.K), 0.0), vEP);
+          }
+          if (kEC_) comp_add(ts[kEC], tc[kEC], vEC);
+          if (kEP_) comp_add(ts[kEP], tc[kEP], vEP);
+        }
+      }
+
+      if (CNT) {
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          // leaf bookkeeping (K6): leaves per total up count, code coverage
+          const unsigned long long node = (tp << sc.m) | (unsigned long long)(j0 + p);
+#pragma unroll
+          for (int c = 0; c < NC; ++c) atomicAdd(&shist[hn[p] + c], (unsigned long long)binom(L, c));
+          leaves += 1ull << L;
+          // sum of codes node*2^L + s, s < 2^L
+          code_sum += (node << (2 * L)) + (((1ull << L) * ((1ull << L) - 1)) >> 1);
+        }
+      }
+    }
    }  // rr
     // --- per-unit partial: fixed warp tree, lane 0 stores
 #pragma unroll
