@@ -152,6 +152,10 @@ def value_exact_parallel(req) -> float:
     """Partitioned enumeration (exact.py:112-133) -- on the GPU(s)."""
     if not _positive_int(req.workers):
         raise InvalidWorkerCount(f"workers must be a positive integer, got {req.workers!r}")
+    _check_enumerable(req)
+    n = int(req.inputs.N)
+    if req.workers > (1 << n):  # make_partition's bound (paths.py:117-120), checked before any launch
+        raise InvalidWorkerCount(f"worker count {req.workers} exceeds the {1 << n} paths of an {n}-step tree")
     return _single(req)
 
 

@@ -98,6 +98,8 @@ def test_guard_and_validation_fire_before_any_launch():
         bp.value_exact_parallel(_req(40, workers=8))
     with pytest.raises(bp.InvalidWorkerCount):
         _req(10, workers=0)
+    with pytest.raises(bp.InvalidWorkerCount):  # make_partition's m <= 2^N bound (paths.py:115-118)
+        bp.value_exact_parallel(_req(2, workers=5))
     with pytest.raises(bp.LengthMismatch):
         bp.ValuationRequest(inputs=bp.MarketInputs(S0=1.0, K=1.0, q=0.0, sigma=0.2, T=1.0, N=5),
                             params=bp.classic_crr(4, 0.2, 0.0, 1.0), kind=bp.ASIAN_CALL)
