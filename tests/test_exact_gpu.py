@@ -232,3 +232,29 @@ def test_per_step_probabilities_weighted_engine(N):
     for k in ALL:
         assert _close(a.values[k], want[k]), (N, k, a.values[k], want[k])
         assert _close(b.values[k], want[k]), (N, k, b.values[k], want[k])
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_fuzz_general_lattices_vs_oracle(seed):
+    """Seeded fuzz over lattices the BASELINE configs do not reach: d != 1/u,
+    p near 0 or 1, deep in/out of the money strikes; the leaf engine (K1),
+    the threshold-search engine (K8) and the oracle must agree (1e-12)."""
+    rng = np.random.default_rng(1000 + seed)
+    N = int(rng.integers(16, 23))
+    u = float(rng.uniform(1.005, 1.25))
+    d = float(rng.uniform(0.75, 0.999)) if seed % 2 else 1.0 / u
+    p = float(rng.choice([rng.uniform(0.01, 0.05), rng.uniform(0.2, 0.8), rng.uniform(0.95, 0.99)]))
+    S0 = float(rng.uniform(10, 200))
+    K = float(S0 * rng.choice([0.3, rng.uniform(0.9, 1.1), 2.5]))
+    q, T = float(rng.uniform(-0.02, 0.1)), float(rng.uniform(0.1, 4.0))
+    req = _req(N, S0, K, q, T, u, d, p)
+    kinds = [bp.resolve_kind(k) for k in ALL]
+    res = bp.value_exact(req, kinds=kinds, count=True)
+    assert res.engine == "affine-threshold"
+    want = oracle.exact(N, S0, K, u, d, p, math.exp(-q * T), ALL, workers=16)
+    for k in ALL:
+        assert _close(res.values[k], want[k]), (seed, N, k, res.values[k], want[k])
+    assert [int(x) for x in res.hist] == [math.comb(N, h) for h in range(N + 1)]
+    srch = bp.value_exact(req, kinds=[bp.ASIAN_CALL, bp.FLOATING_LOOKBACK], search=True)
+    for k in ("asian-call", "float-lookback"):
+        assert _close(srch.values[k], want[k]), (seed, "search", k, srch.values[k], want[k])
