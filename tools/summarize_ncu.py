@@ -23,6 +23,10 @@ KEYS = [
     ("smsp__inst_executed.sum", "warp instructions", 1),
     ("dram__bytes_read.sum", "DRAM read", 1),
     ("dram__bytes_write.sum", "DRAM write", 1),
+    ("smsp__thread_inst_executed_per_inst_executed.ratio", "active threads per warp instruction (divergence)", 1),
+    ("smsp__sass_average_branch_targets_threads_uniform.pct", "uniform branch targets %", 1),
+    ("smsp__sass_inst_executed_op_local_ld.sum", "local (spill) loads, warp inst", 1),
+    ("smsp__sass_inst_executed_op_local_st.sum", "local (spill) stores, warp inst", 1),
     ("smsp__average_warps_issue_stalled_not_selected_per_issue_active.ratio", "stall not_selected", 1),
     ("smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio", "stall math_pipe", 1),
     ("smsp__average_warps_issue_stalled_mio_throttle_per_issue_active.ratio", "stall mio", 1),
