@@ -90,9 +90,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return OUT
 
 
-def build_variant(name: str, defines, parts=None, all_units: bool = False) -> str:
+def build_variant(name: str, defines, parts=None, all_units: bool = False, sources=None) -> str:
     """Diagnostics: the library with extra -D flags on the K1 instantiation
-    parts (all parts, or the listed ones; every unit with all_units=True)
+    parts (all parts, or the listed ones; every unit with all_units=True; the
+    units of the listed source basenames with sources=[...])
     -> _lib/variants/<name>.so, for
     BINPATHS_LIB=... scans (tools/scan_variants.sh).  Other objects are
     shared with the main build."""
@@ -104,7 +105,11 @@ def build_variant(name: str, defines, parts=None, all_units: bool = False) -> st
     objs, procs = [], []
     for src, extra, obj in units():
         part = next((int(e.split("=")[1]) for e in extra if e.startswith("-DBP_FAST_PART=")), None)
-        if not all_units and (part is None or (parts is not None and part not in parts)):
+        if sources is not None:
+            chosen = os.path.basename(src) in sources
+        else:
+            chosen = all_units or (part is not None and (parts is None or part in parts))
+        if not chosen:
             objs.append(obj)
             continue
         vobj = os.path.join(vdir, os.path.basename(obj))
