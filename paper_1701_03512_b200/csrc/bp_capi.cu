@@ -514,6 +514,15 @@ static int cached_occupancy_fast(int L, unsigned km, bool cnt) {
   return occ;
 }
 
+// BINPATHS_TRACE=1: host-side phase timings on stderr (diagnostics)
+static bool trace_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("BINPATHS_TRACE");
+    return e && std::atoi(e) != 0;
+  }();
+  return on;
+}
+
 static int device_sm_count(int dev) {
   static std::atomic<int> memo[64];
   if (dev >= 0 && dev < 64 && memo[dev].load() > 0) return memo[dev].load();
@@ -737,7 +746,12 @@ static int plan_enqueue(bp_exact_plan* P, int dev, int sb_first, int sb_count, d
       set_units(g.args, lay.L, u0, u1);
       const int occ = std::max(1, cached_occupancy_fast(lay.L, g.km, cnt_g));
       const int grid = (int)std::max<unsigned long long>(1, std::min<unsigned long long>(want, (unsigned long long)occ * sms));
+      const auto tl0 = std::chrono::steady_clock::now();
       BP_CUDA(launch_exact_fast(lay.L, g.km, g.args.data(), cnt_g, grid, st, unit_base, hist_dev));
+      const auto tl1 = std::chrono::steady_clock::now();
+      if (trace_on())
+        std::fprintf(stderr, "[bp trace] K1 launch %.1f us (%zu B of arguments)\n",
+                     std::chrono::duration<double, std::micro>(tl1 - tl0).count(), g.args.size());
       BP_CUDA(launch_sb_reduce(unit_base, lay.units_per_sb, sb_first, sb_count, g.km, std::exchange(zero_kinds, 0u), 1.0 / P->tree.n_steps,
                                out_dev, st));
     }
@@ -925,10 +939,7 @@ static void run_device_job(const bp_tree* t, uint32_t payoffs, uint32_t flags, D
   if (cnt) cudaMemsetAsync(c.hist_dev, 0, sizeof(unsigned long long) * 66, c.st);
   keep_pool(job->device);
   // host preparation (tables) happens before the timed window
-  static const bool trace = [] {
-    const char* e = std::getenv("BINPATHS_TRACE");
-    return e && std::atoi(e) != 0;
-  }();
+  const bool trace = trace_on();
   using clk = std::chrono::steady_clock;
   const auto t0 = clk::now();
   bp_exact_plan P;
