@@ -90,6 +90,20 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return OUT
 
 
+def build_example() -> str:
+    """examples/bp_price.c: a plain C client of the C ABI (header + .so only)."""
+    root = os.path.dirname(HERE)
+    src = os.path.join(root, "examples", "bp_price.c")
+    out = os.path.join(root, "examples", "bp_price")
+    lib = build()
+    if os.path.exists(out) and os.path.getmtime(out) >= max(os.path.getmtime(src), os.path.getmtime(lib)):
+        return out
+    subprocess.check_call([os.environ.get("CC", "cc"), "-O2", "-std=c11", "-Wall", "-I", os.path.join(root, "include"),
+                           src, "-o", out, "-L", os.path.dirname(lib), "-lbinpaths_b200",
+                           "-Wl,-rpath,$ORIGIN/../paper_1701_03512_b200/_lib", "-lm"])
+    return out
+
+
 def build_variant(name: str, defines, parts=None, all_units: bool = False, sources=None) -> str:
     """Diagnostics: the library with extra -D flags on the K1 instantiation
     parts (all parts, or the listed ones; every unit with all_units=True; the

@@ -57,3 +57,12 @@ def test_host_side_abi_functions_without_gpu():
         res = _native.BpExactResult()
         rc = L.bp_exact(ctypes.byref(t), 1 << 4, 0, 0, None, ctypes.byref(res))
         assert rc == 101
+
+
+def test_plain_c_client_builds_against_header_and_library():
+    """examples/bp_price.c compiles and links against include/binpaths_b200.h
+    and the built .so alone (runs on the GPU box, tests/test_c_client_gpu.py)."""
+    import os
+    from paper_1701_03512_b200 import build as b
+    exe = b.build_example()
+    assert os.access(exe, os.X_OK)
