@@ -9,6 +9,7 @@
 // share of the option's thread prefixes, nodes in pairs.  Partials are
 // reduced in a fixed order (CTA tree, then ascending CTA index per option).
 #include <cmath>
+#include <cstdlib>
 #include "bp_kernels.h"
 #include "bp_leaf.cuh"
 
@@ -202,6 +203,11 @@ __global__ void k_batch_combine(const double2* __restrict__ partial, int n_opts,
 }
 
 int batch_ctas_per_option(int n_opts) {
+  static const int forced = [] {
+    const char* e = std::getenv("BINPATHS_BATCH_CPO_LOG2");  // diagnostics
+    return e ? std::atoi(e) : -1;
+  }();
+  if (forced >= 0) return forced;
   // enough CTAs to fill 148 SMs x 3 resident CTAs, at most 16 per option
   int l = 0;
   while (l < 4 && (long long)n_opts << l < 148 * 3) ++l;
