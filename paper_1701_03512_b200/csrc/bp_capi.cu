@@ -903,6 +903,18 @@ struct DevCtx {
   unsigned long long* hist_host = nullptr; // pinned
   double2* scratch = nullptr;              // unit partials, grown on demand, kept
   size_t scratch_bytes = 0;
+  // CUDA graphs of repeated synchronous valuations (class engine): key =
+  // everything the captured launches depend on, most recent first
+  struct Graph {
+    std::vector<unsigned char> key;
+    cudaGraphExec_t exec = nullptr;
+  };
+  std::list<Graph> graphs;
+  void drop_graphs() {
+    for (auto& g : graphs)
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+    graphs.clear();
+  }
 };
 static DevCtx g_ctx[64];
 
@@ -919,6 +931,89 @@ static cudaError_t ctx_init(DevCtx& c, int dev) {
   if ((e = cudaMallocHost((void**)&c.hist_host, sizeof(unsigned long long) * 66)) != cudaSuccess) return e;
   c.ready = true;
   return cudaSuccess;
+}
+
+static bool graphs_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("BINPATHS_GRAPH");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
+// the timing events sit outside the graph (kernel_ms then also holds the
+// 768-byte result copy at the graph's end)
+static bool launch_graph(DevCtx& c, cudaGraphExec_t exec) {
+  cudaEventRecord(c.e0, c.st);
+  const bool ok = cudaGraphLaunch(exec, c.st) == cudaSuccess;
+  cudaEventRecord(c.e1, c.st);
+  return ok;
+}
+
+// Synchronous class-engine valuation as ONE graph launch: K1 (one per kind
+// group), K2 and the partials' D2H copy.  The graph is captured on
+// the first call for a given (argument blocks, layout, super-block range,
+// scratch); a repeated valuation -- the same contract, e.g. a revaluation loop
+// or the bench's e2e -- replays it (~5 us of host work instead of ~20 us of
+// launches with 12 KB of kernel arguments).  Returns false to take the
+// ordinary launch path (other engines, bookkeeping, or any capture failure).
+static bool try_graph_job(DevCtx& c, bp_exact_plan& P, DeviceJob* job, uint32_t flags, bool cnt) {
+  if (!graphs_enabled() || cnt || P.lay.engine != 1) return false;
+  const int dev = job->device;
+  const unsigned long long n_units = (unsigned long long)job->sb_count * P.lay.units_per_sb;
+  const size_t need = sizeof(double2) * kNumKinds * n_units;
+  if (c.scratch_bytes < need) {  // size the scratch outside any capture; graphs on the old buffer go
+    c.drop_graphs();
+    if (c.scratch) cudaFreeAsync(c.scratch, c.st);
+    c.scratch = nullptr;
+    c.scratch_bytes = 0;
+    if (cudaMallocAsync((void**)&c.scratch, need, c.st) != cudaSuccess) return false;
+    c.scratch_bytes = need;
+  }
+  for (auto& g : P.groups) cached_occupancy_fast(P.lay.L, g.km, false);  // no queries inside the capture
+  std::vector<unsigned char> key;
+  auto put = [&key](const void* p, size_t n) {
+    const auto* b = static_cast<const unsigned char*>(p);
+    key.insert(key.end(), b, b + n);
+  };
+  put(&P.lay, sizeof(P.lay));
+  put(&P.payoffs, sizeof(P.payoffs));
+  put(&flags, sizeof(flags));
+  put(&job->sb_first, sizeof(int));
+  put(&job->sb_count, sizeof(int));
+  put(&c.scratch, sizeof(c.scratch));
+  for (auto& g : P.groups) {
+    put(&g.km, sizeof(g.km));
+    put(g.args.data(), g.args.size());
+  }
+  const size_t np = (size_t)job->sb_count * BP_N_PAYOFFS * 2;
+  for (auto it = c.graphs.begin(); it != c.graphs.end(); ++it)
+    if (it->key == key) {
+      c.graphs.splice(c.graphs.begin(), c.graphs, it);
+      return launch_graph(c, it->exec);
+    }
+  cudaGraph_t graph = nullptr;
+  if (cudaStreamBeginCapture(c.st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) return false;
+  P.scratch[dev].p = c.scratch;
+  P.scratch[dev].bytes = c.scratch_bytes;
+  int rc = plan_enqueue(&P, dev, job->sb_first, job->sb_count, c.out_dev, nullptr, c.st);
+  P.scratch[dev].p = nullptr;
+  P.scratch[dev].bytes = 0;
+  cudaMemcpyAsync(c.out_host, c.out_dev, sizeof(double) * np, cudaMemcpyDeviceToHost, c.st);
+  const cudaError_t ec = cudaStreamEndCapture(c.st, &graph);
+  cudaGraphExec_t exec = nullptr;
+  if (rc || ec != cudaSuccess || !graph || cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();  // clear a capture error; the caller takes the ordinary path
+    return false;
+  }
+  cudaGraphDestroy(graph);
+  c.graphs.push_front(DevCtx::Graph{std::move(key), exec});
+  if (c.graphs.size() > 8) {
+    cudaGraphExecDestroy(c.graphs.back().exec);
+    c.graphs.pop_back();
+  }
+  return launch_graph(c, exec);
 }
 
 static void run_device_job(const bp_tree* t, uint32_t payoffs, uint32_t flags, DeviceJob* job) {
@@ -951,6 +1046,17 @@ static void run_device_job(const bp_tree* t, uint32_t payoffs, uint32_t flags, D
       e = cudaMemcpyAsync(P.th_dev[job->device], P.th_tables.data(), sizeof(double) * P.th_tables.size(),
                           cudaMemcpyHostToDevice, c.st);
     if (e != cudaSuccess) return cuda_fail(e, "threshold tables");
+  }
+  if (!rc && try_graph_job(c, P, job, flags, cnt)) {  // class engine, repeated valuation: one graph launch
+    const auto t2 = clk::now();
+    if ((e = cudaStreamSynchronize(c.st)) != cudaSuccess) return cuda_fail(e, "valuation (graph)");
+    if (trace)
+      std::fprintf(stderr, "[bp trace] dev %d: plan %.1f us, graph launch %.1f us\n", job->device,
+                   std::chrono::duration<double, std::micro>(t1 - t0).count(),
+                   std::chrono::duration<double, std::micro>(t2 - t1).count());
+    std::memcpy(job->partials.data(), c.out_host, sizeof(double) * np);
+    cudaEventElapsedTime(&job->ms, c.e0, c.e1);
+    return;
   }
   cudaEventRecord(c.e0, c.st);
   P.scratch[job->device].p = c.scratch;  // the context's buffer (plan_enqueue grows it if needed)

@@ -4,6 +4,7 @@ Bar (BASELINE.json north_star): exact values within 1e-12 relative; leaf
 bookkeeping (paths per up count, total, code checksum) bit-exact.
 """
 import math
+import os
 
 import numpy as np
 import pytest
@@ -258,3 +259,33 @@ def test_fuzz_general_lattices_vs_oracle(seed):
     srch = bp.value_exact(req, kinds=[bp.ASIAN_CALL, bp.FLOATING_LOOKBACK], search=True)
     for k in ("asian-call", "float-lookback"):
         assert _close(srch.values[k], want[k]), (seed, "search", k, srch.values[k], want[k])
+
+
+def test_graph_replay_is_bitwise_the_launch_path():
+    """Repeated synchronous valuations replay a captured CUDA graph (bp_capi.cu
+    try_graph_job); the values must be bitwise those of the ordinary launch
+    path (BINPATHS_GRAPH=0, a fresh process) and stable across replays and
+    across contracts sharing the lattice."""
+    import json
+    import subprocess
+    import sys
+    from conftest import ROOT
+    code = ("import json, paper_1701_03512_b200 as bp\n"
+            "P = bp.classic_crr(26, 0.2, 0.05, 1.0)\n"
+            "out = []\n"
+            "for K in (95.0, 105.0, 95.0):\n"
+            "    inp = bp.MarketInputs(S0=100.0, K=K, q=0.05, sigma=0.2, T=1.0, N=26)\n"
+            "    req = bp.ValuationRequest(inputs=inp, params=P, kind=bp.ASIAN_CALL, force_large=True)\n"
+            "    for _ in range(3):\n"
+            "        out.append(bp.value_exact(req, kinds=[bp.ASIAN_CALL, bp.FLOATING_LOOKBACK]).values)\n"
+            "print(json.dumps([[v.hex() for v in d.values()] for d in out]))\n")
+    runs = {}
+    for flag in ("1", "0"):
+        env = dict(os.environ, BINPATHS_GRAPH=flag)
+        p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, cwd=ROOT,
+                           timeout=300)
+        assert p.returncode == 0, p.stderr
+        runs[flag] = json.loads(p.stdout.strip().splitlines()[-1])
+    assert runs["1"] == runs["0"]
+    r = runs["1"]
+    assert r[0] == r[1] == r[2] == r[6] == r[7] == r[8] and r[3] == r[4] == r[5] and r[0] != r[3]
