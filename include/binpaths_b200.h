@@ -22,6 +22,8 @@
  *                        (pkg/src/binpaths/mc.py:197-213, sampler
  *                        mc.py:92-100); with r = 0 it is estimate_basic's
  *                        draw loop (mc.py:135-159)
+ *   bp_mc_range          _stratum_stats over draw slices (one process per
+ *                        GPU: basic MC's draws split by rank)
  *   bp_mc_shared         the draw loop of estimate_shared (mc.py:287-331)
  *   bp_philox4x32_10     counter-based generator used by bp_mc_* (stands in
  *                        for numpy Philox keyed by SeedSequence, mc.py:92-95)
@@ -168,6 +170,18 @@ int bp_mc_strata(const bp_tree* tree, uint32_t payoff, int r,
  * on the stratum-0 stream, each evaluated under all 2^r prefixes; inner =
  * sum_m masses[m] * payoff(m, draw).  Writes, per repetition, the mean and
  * sse of the inner sums and the per-stratum payoff means ([n_reps][2^r]). */
+/* bp_mc_strata over draw RANGES: stratum m contributes draws
+ * [first[m], end[m]) of its stream (same draws as in the full run).  It
+ * writes the range's mean and sum of squared deviations (mean, m2; count =
+ * end - first) per stratum and repetition.  For one process per GPU: a
+ * range starting at a multiple of 4096 draws is evaluated exactly as in the
+ * full run; the ranks' (count, mean, m2) are merged with Chan's formula in
+ * rank order.  Replaces _stratum_stats over a slice of draws (mc.py:197-213). */
+int bp_mc_range(const bp_tree* tree, uint32_t payoff, int r,
+                const uint64_t* first, const uint64_t* end, uint64_t seed,
+                uint32_t rep0, uint32_t n_reps, int device, double* mean,
+                double* m2, double* kernel_ms);
+
 int bp_mc_shared(const bp_tree* tree, uint32_t payoff, int r, uint64_t R,
                  const double* masses, uint64_t seed, uint32_t rep0,
                  uint32_t n_reps, int device, double* inner_mean,

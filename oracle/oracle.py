@@ -49,6 +49,8 @@ def lib():
         L.orc_philox4x32_10.restype = None
         L.orc_mc_strata.argtypes = [i, d, d, d, d, pd, i, i, pu64, u64, ctypes.c_uint32, ctypes.c_uint32, pd, pd]
         L.orc_mc_strata.restype = i
+        L.orc_mc_range.argtypes = [i, d, d, d, d, pd, i, i, pu64, pu64, u64, ctypes.c_uint32, ctypes.c_uint32, pd, pd]
+        L.orc_mc_range.restype = i
         L.orc_mc_shared.argtypes = [i, d, d, d, d, pd, i, i, u64, pd, u64, ctypes.c_uint32, ctypes.c_uint32,
                                     pd, pd, pd]
         L.orc_mc_shared.restype = i
@@ -111,6 +113,20 @@ def mc_strata(N, S0, K, u, d, probs, kind, r, draws, seed, rep0=0, n_reps=1):
                         draws.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), seed, rep0, n_reps,
                         _dp(theta), _dp(sse))
     return theta.reshape(n_reps, M), sse.reshape(n_reps, M)
+
+
+def mc_range(N, S0, K, u, d, probs, kind, r, first, end, seed, rep0=0, n_reps=1):
+    """Per-stratum (mean, M2) over draws [first[m], end[m]) (bp_mc_range)."""
+    probs = _probs(N, probs)
+    first = np.ascontiguousarray(first, dtype=np.uint64)
+    end = np.ascontiguousarray(end, dtype=np.uint64)
+    M = 1 << r
+    mean = np.zeros(n_reps * M)
+    m2 = np.zeros(n_reps * M)
+    lib().orc_mc_range(N, S0, K, u, d, _dp(probs), KIND_BITS[kind], r,
+                       first.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+                       end.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), seed, rep0, n_reps, _dp(mean), _dp(m2))
+    return mean.reshape(n_reps, M), m2.reshape(n_reps, M)
 
 
 def mc_shared(N, S0, K, u, d, probs, kind, r, R, masses, seed, rep0=0, n_reps=1):

@@ -69,7 +69,7 @@ class BpExactResult(ctypes.Structure):
 # every symbol the header declares (tests check the .so exports all of them)
 EXPORTED = (
     "bp_exact", "bp_exact_layout", "bp_exact_superblocks", "bp_combine_superblocks", "bp_exact_batch",
-    "bp_mc_strata", "bp_mc_shared", "bp_philox4x32_10", "bp_fp64_peak", "bp_device_count",
+    "bp_mc_strata", "bp_mc_range", "bp_mc_shared", "bp_philox4x32_10", "bp_fp64_peak", "bp_device_count",
     "bp_abi_version", "bp_last_error", "bp_exact_plan_create", "bp_exact_plan_layout", "bp_exact_plan_enqueue",
     "bp_exact_plan_destroy",
 )
@@ -114,6 +114,8 @@ def _declare(L):
     L.bp_exact_batch.argtypes = [P(BpTree), c_int, c_u32, c_int, P(c_dbl), P(c_dbl)]
     L.bp_mc_strata.argtypes = [P(BpTree), c_u32, c_int, P(c_u64), c_u64, c_u32, c_u32, c_int, P(c_dbl),
                                P(c_dbl), P(c_dbl)]
+    L.bp_mc_range.argtypes = [P(BpTree), c_u32, c_int, P(c_u64), P(c_u64), c_u64, c_u32, c_u32, c_int, P(c_dbl),
+                              P(c_dbl), P(c_dbl)]
     L.bp_mc_shared.argtypes = [P(BpTree), c_u32, c_int, c_u64, P(c_dbl), c_u64, c_u32, c_u32, c_int, P(c_dbl),
                                P(c_dbl), P(c_dbl), P(c_dbl)]
     L.bp_philox4x32_10.argtypes = [P(ctypes.c_uint32), P(ctypes.c_uint32), P(ctypes.c_uint32)]

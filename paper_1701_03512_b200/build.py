@@ -28,11 +28,21 @@ def deps():
                               [os.path.join(HERE, "..", "include", "binpaths_b200.h")])
 
 
+def _stale_units(force: bool = False) -> list:
+    """Units whose object is missing or older than its source or any header."""
+    headers = [d for d in deps() if not d.endswith(".cu")]
+    newest_header = max(os.path.getmtime(h) for h in headers)
+    return [u for u in units() if force or not os.path.exists(u[2]) or
+            os.path.getmtime(u[2]) < max(newest_header, os.path.getmtime(u[0]))]
+
+
 def up_to_date() -> bool:
-    if not os.path.exists(OUT):
+    """Per object, not per library: a library linked from objects compiled
+    before a later source edit is stale even if it is newer than the edit."""
+    if not os.path.exists(OUT) or _stale_units():
         return False
     t = os.path.getmtime(OUT)
-    return all(os.path.getmtime(p) <= t for p in deps())
+    return all(os.path.getmtime(u[2]) <= t for u in units())
 
 
 def fast_parts() -> int:
@@ -73,11 +83,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return subprocess.call(cmd)
 
     # incremental: an object is rebuilt when its source or any header is newer
-    headers = [d for d in deps() if not d.endswith(".cu")]
-    newest_header = max(os.path.getmtime(h) for h in headers)
     all_units = units()
-    todo = [u for u in all_units if force or not os.path.exists(u[2]) or
-            os.path.getmtime(u[2]) < max(newest_header, os.path.getmtime(u[0]))]
+    todo = _stale_units(force)
     with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
         rcs = list(ex.map(run, todo))
     failed = [u[0] + " " + " ".join(u[1]) for u, rc in zip(todo, rcs) if rc != 0]

@@ -1226,8 +1226,12 @@ struct DevBuf {
   }
 };
 
-extern "C" int bp_mc_strata(const bp_tree* tree, uint32_t payoff, int r, const uint64_t* draws, uint64_t seed,
-                            uint32_t rep0, uint32_t n_reps, int device, double* theta, double* sse,
+// Stratified MC over draw ranges [first[m], end[m]) of every stratum (first
+// == nullptr: [0, end[m])).  Work items are chunks of mc_chunk() draws
+// starting at first[m], so a range starting at a multiple of the chunk has
+// exactly the items (and per-item statistics) of the full-range run.
+static int mc_strata_ranges(const bp_tree* tree, uint32_t payoff, int r, const uint64_t* first, const uint64_t* draws,
+                            uint64_t seed, uint32_t rep0, uint32_t n_reps, int device, double* theta, double* sse,
                             double* kernel_ms) {
   int rc = validate_tree(tree, 64);
   if (rc) return rc;
@@ -1237,14 +1241,16 @@ extern "C" int bp_mc_strata(const bp_tree* tree, uint32_t payoff, int r, const u
   if (!draws || !theta || !sse || n_reps < 1) return fail(BP_E_INVALID_INPUT, "bad Monte Carlo buffers");
   if (device < 0 || device >= bp_device_count()) return fail(BP_E_NO_DEVICE, "no CUDA device " + std::to_string(device));
   const int M = 1 << r;
-  for (int m = 0; m < M; ++m)
+  for (int m = 0; m < M; ++m) {
     if (draws[m] >= (1ull << 32)) return fail(BP_E_INVALID_INPUT, "at most 2^32 - 1 draws per stratum");
+    if (first && first[m] > draws[m]) return fail(BP_E_INVALID_INPUT, "draw range with first > end");
+  }
   // work items of one repetition, stratum-ascending
   const unsigned long long CH = mc_chunk();
   std::vector<unsigned long long> item_stratum, item_first, stratum_item0(M + 1, 0);
   for (int m = 0; m < M; ++m) {
     stratum_item0[m] = item_stratum.size();
-    for (unsigned long long f = 0; f < draws[m]; f += CH) {
+    for (unsigned long long f = first ? first[m] : 0; f < draws[m]; f += CH) {
       item_stratum.push_back(m);
       item_first.push_back(f);
     }
@@ -1300,6 +1306,19 @@ extern "C" int bp_mc_strata(const bp_tree* tree, uint32_t payoff, int r, const u
   cudaEventDestroy(e1);
   if (kernel_ms) *kernel_ms = ms;
   return BP_OK;
+}
+
+extern "C" int bp_mc_strata(const bp_tree* tree, uint32_t payoff, int r, const uint64_t* draws, uint64_t seed,
+                            uint32_t rep0, uint32_t n_reps, int device, double* theta, double* sse,
+                            double* kernel_ms) {
+  return mc_strata_ranges(tree, payoff, r, nullptr, draws, seed, rep0, n_reps, device, theta, sse, kernel_ms);
+}
+
+extern "C" int bp_mc_range(const bp_tree* tree, uint32_t payoff, int r, const uint64_t* first, const uint64_t* end,
+                           uint64_t seed, uint32_t rep0, uint32_t n_reps, int device, double* mean, double* m2,
+                           double* kernel_ms) {
+  if (!first) return fail(BP_E_INVALID_INPUT, "bp_mc_range needs the first draw of every stratum");
+  return mc_strata_ranges(tree, payoff, r, first, end, seed, rep0, n_reps, device, mean, m2, kernel_ms);
 }
 
 extern "C" int bp_mc_shared(const bp_tree* tree, uint32_t payoff, int r, uint64_t R, const double* masses,

@@ -137,3 +137,168 @@ def value_exact_distributed(req, kinds: Optional[Sequence] = None, rank: int = 0
     sh.enqueue()
     sh.exchange(group)
     return sh.values()
+
+
+# ---------------------------------------------------------------------------
+# Monte Carlo and batched pricing, one process per GPU.
+#
+# * Stratified MC with M >= G strata: rank g owns the contiguous strata range
+#   of shard_range(M, g, G) -- the top log2 G bits of the k-bit prefix -- and
+#   runs exactly the single-GPU work for them (same draws, same work items,
+#   same per-stratum merge), so after the all_gather every stratum's
+#   (theta_m, SSE_m) is bitwise the single-GPU value; the host combine
+#   (mc._partitioned_from, ascending m) is unchanged.
+# * M < G (basic MC, M = 1): every stratum's draws are split into G
+#   contiguous, chunk-aligned ranges (bp_mc_range); the ranks' (n, mean, M2)
+#   are merged with Chan's formula in rank order.  Equal to the single-GPU
+#   statistics up to the association of that merge (~1e-15 relative).
+# * Batched exact pricing: contiguous option slices, one all_gather.
+
+def _gather_np(arr: np.ndarray, world: int, group=None) -> np.ndarray:
+    """all_gather of an equal-shape float64 array -> [world, *shape] (NCCL on
+    the current CUDA device, or gloo on CPU for the host-logic tests)."""
+    import torch
+    import torch.distributed as dist
+
+    backend = dist.get_backend(group)
+    dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
+    arr = np.ascontiguousarray(arr, dtype=np.float64)
+    local = torch.from_numpy(arr.reshape(-1)).to(dev)
+    out = torch.empty(world * local.numel(), dtype=torch.float64, device=dev)
+    dist.all_gather_into_tensor(out, local, group=group)  # concatenated along dim 0
+    return out.cpu().numpy().reshape((world,) + arr.shape)
+
+
+def chunk_ranges(R: int, world: int, chunk: int) -> list:
+    """[first, end) draw ranges of the G ranks: contiguous, starting at
+    multiples of the engine's work-item size (so each rank's items are the
+    single-GPU items), as balanced as the chunking allows."""
+    n_chunks = -(-R // chunk) if R else 0
+    out = []
+    for g in range(world):
+        c0, cn = (shard_range(n_chunks, g, world) if n_chunks >= world
+                  else ((g, 1) if g < n_chunks else (n_chunks, 0)))
+        out.append((min(c0 * chunk, R), min((c0 + cn) * chunk, R)))
+    return out
+
+
+def chan_merge(parts) -> tuple:
+    """Fixed-order (rank order) Chan merge of (n, mean, M2) triples."""
+    n, mean, m2 = 0.0, 0.0, 0.0
+    for nb, mb, m2b in parts:
+        if nb == 0:
+            continue
+        if n == 0:
+            n, mean, m2 = float(nb), float(mb), float(m2b)
+            continue
+        tot = n + nb
+        delta = mb - mean
+        f = nb / tot
+        mean = mean + delta * f
+        m2 = m2 + m2b + delta * delta * n * f
+        n = tot
+    return n, mean, m2
+
+
+def make_sharded_stats(rank: int, world: int, device: Optional[int] = None, group=None, compute=None):
+    """A drop-in for mc._strata_stats that shards the work over `world`
+    processes.  compute(req, r, first, end, seed, rep0, n_reps) -> (mean, m2)
+    arrays [n_reps, 2^r] over draw ranges defaults to the GPU (bp_mc_range);
+    the CPU host-logic tests pass the oracle."""
+    from . import mc as _mc
+
+    def native_compute(req, r, first, end, seed, rep0, n_reps):
+        tree, keep = _mc._tree(req)
+        M = 1 << r
+        f = np.ascontiguousarray(first, dtype=np.uint64)
+        e = np.ascontiguousarray(end, dtype=np.uint64)
+        mean, m2 = np.zeros(n_reps * M), np.zeros(n_reps * M)
+        ms = ctypes.c_double()
+        dev = _mc._device(req) if device is None else device
+        _native.check(_native.lib().bp_mc_range(ctypes.byref(tree), 1 << kind_bit(req.kind), r, _native.u64ptr(f),
+                                                _native.u64ptr(e), seed, rep0, n_reps, dev, _native.dptr(mean),
+                                                _native.dptr(m2), ctypes.byref(ms)))
+        del keep
+        return mean.reshape(n_reps, M), m2.reshape(n_reps, M)
+
+    run = compute or native_compute
+
+    def stats(req, r, draws, seed, rep0, n_reps):
+        M = 1 << r
+        draws = np.asarray(draws, dtype=np.uint64)
+        if M >= world:  # strata shard: bitwise the single-GPU per-stratum statistics
+            s0, cnt = shard_range(M, rank, world)
+            end = np.zeros(M, dtype=np.uint64)
+            end[s0:s0 + cnt] = draws[s0:s0 + cnt]
+            mean, m2 = run(req, r, np.zeros(M, dtype=np.uint64), end, seed, rep0, n_reps)
+            both = _gather_np(np.stack([mean, m2]), world, group) if world > 1 else np.stack([mean, m2])[None]
+            theta, sse = np.zeros((n_reps, M)), np.zeros((n_reps, M))
+            for g in range(world):
+                a, c = shard_range(M, g, world)
+                theta[:, a:a + c] = both[g, 0][:, a:a + c]
+                sse[:, a:a + c] = both[g, 1][:, a:a + c]
+            return theta, sse, 0.0
+        # draw shard: every stratum's draws split by rank, Chan merge in rank order
+        chunk = _native_chunk()
+        rng = [chunk_ranges(int(R), world, chunk) for R in draws]
+        first = np.array([rng[m][rank][0] for m in range(M)], dtype=np.uint64)
+        end = np.array([rng[m][rank][1] for m in range(M)], dtype=np.uint64)
+        mean, m2 = run(req, r, first, end, seed, rep0, n_reps)
+        local = np.stack([mean, m2])
+        both = _gather_np(local, world, group) if world > 1 else local[None]
+        theta, sse = np.zeros((n_reps, M)), np.zeros((n_reps, M))
+        for k in range(n_reps):
+            for m in range(M):
+                parts = [(rng[m][g][1] - rng[m][g][0], both[g, 0][k, m], both[g, 1][k, m]) for g in range(world)]
+                _, theta[k, m], sse[k, m] = chan_merge(parts)
+        return theta, sse, 0.0
+
+    return stats
+
+
+def _native_chunk() -> int:
+    return 4096  # csrc/bp_mc_kernels.cu kChunk (work-item size in draws)
+
+
+def run_repetitions_distributed(estimator, req, cfg, rank: int, world: int, device: Optional[int] = None,
+                                group=None, compute=None):
+    """mc.run_repetitions with the draws sharded over `world` processes (one
+    GPU each); every rank returns the same RepetitionSummary.  Supports
+    estimate_basic, estimate_partitioned and estimate_partitioned_equal (the
+    shared-sample estimator evaluates one suffix sample under all strata and
+    is not sharded here)."""
+    from . import mc as _mc
+
+    table = {_mc.estimate_basic: _mc._basic_reps, _mc.estimate_partitioned: _mc._partitioned_reps,
+             _mc.estimate_partitioned_equal: _mc._equal_reps}
+    if estimator not in table:
+        from .errors import InvalidInput
+        raise InvalidInput(f"{getattr(estimator, '__name__', estimator)} is not sharded across processes")
+    stats = make_sharded_stats(rank, world, device, group, compute)
+    estimates = tuple(table[estimator](req, cfg, 0, cfg.reps, stats=stats))
+    values = np.array([e.value for e in estimates])
+    variances = np.array([e.variance for e in estimates])
+    return _mc.RepetitionSummary(estimates=estimates, mean_value=float(values.mean()),
+                                 mean_variance=float(variances.mean()),
+                                 empirical_variance=float(np.var(values, ddof=1)) if len(estimates) > 1 else 0.0)
+
+
+def price_batch_distributed(N: int, S0, K, u, d, p, disc, kind, rank: int, world: int, device: int = 0, group=None,
+                            compute=None) -> np.ndarray:
+    """exact.price_batch with the options split into contiguous slices, one
+    per process (GPU), and ONE all_gather of the per-option values.  Every
+    rank returns all values in input order (each option's value is the same
+    kernel work as in the single-GPU batch)."""
+    from .exact import price_batch
+
+    arrs = np.broadcast_arrays(*(np.asarray(x, dtype=np.float64) for x in (S0, K, u, d, p, disc)))
+    n = arrs[0].size
+    flat = [a.reshape(-1) for a in arrs]
+    per = -(-n // world)
+    lo, hi = min(rank * per, n), min((rank + 1) * per, n)
+    run = compute or (lambda *a: price_batch(N, *a, kind, device=device))
+    mine = np.zeros(per)
+    if hi > lo:
+        mine[:hi - lo] = run(*(x[lo:hi] for x in flat))
+    allv = _gather_np(mine, world, group) if world > 1 else mine[None]
+    return allv.reshape(-1)[:n]

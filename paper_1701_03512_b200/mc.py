@@ -222,28 +222,28 @@ def _partitioned_from(req, cfg, masses, alloc, thetas, sses, equal: bool) -> Est
                     per_stratum=tuple((m, int(alloc[m]), float(th[m])) for m in range(len(alloc))))
 
 
-def _basic_reps(req, cfg, rep0, n_reps):
+def _basic_reps(req, cfg, rep0, n_reps, stats=None):
     if cfg.R < 2:
         raise InvalidInput(f"basic estimator needs R >= 2, got {cfg.R}")
-    theta, sse, _ = _strata_stats(req, 0, [cfg.R], cfg.seed, rep0, n_reps)
+    theta, sse, _ = (stats or _strata_stats)(req, 0, [cfg.R], cfg.seed, rep0, n_reps)
     return [_basic_from(req, cfg, float(theta[k, 0]), float(sse[k, 0])) for k in range(n_reps)]
 
 
-def _partitioned_reps(req, cfg, rep0, n_reps):
+def _partitioned_reps(req, cfg, rep0, n_reps, stats=None):
     if cfg.R < cfg.M:
         raise InfeasibleAllocation(f"partitioned estimator needs R >= M, got R={cfg.R}, M={cfg.M}")
     part = _stratified_partition(req, cfg.M)
     masses = [block_probability(req.params, part, m) for m in range(cfg.M)]
     alloc = allocate_strata(part, req.params, cfg.R)
-    theta, sse, _ = _strata_stats(req, part.prefix_width, alloc, cfg.seed, rep0, n_reps)
+    theta, sse, _ = (stats or _strata_stats)(req, part.prefix_width, alloc, cfg.seed, rep0, n_reps)
     return [_partitioned_from(req, cfg, masses, alloc, theta[k], sse[k], equal=False) for k in range(n_reps)]
 
 
-def _equal_reps(req, cfg, rep0, n_reps):
+def _equal_reps(req, cfg, rep0, n_reps, stats=None):
     part = _stratified_partition(req, cfg.M)
     masses = [block_probability(req.params, part, m) for m in range(cfg.M)]
     alloc = [cfg.R] * cfg.M
-    theta, sse, _ = _strata_stats(req, part.prefix_width, alloc, cfg.seed, rep0, n_reps)
+    theta, sse, _ = (stats or _strata_stats)(req, part.prefix_width, alloc, cfg.seed, rep0, n_reps)
     return [_partitioned_from(req, cfg, masses, alloc, theta[k], sse[k], equal=True) for k in range(n_reps)]
 
 
