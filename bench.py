@@ -288,7 +288,7 @@ def secondary_configs(dev):
                       "value": (R_m << k) / (t * 1e-3), "unit": "draws/s", "kernel_ms": t,
                       "estimate": e.value, "std_error": e.std_error, "basic_estimate": b.value,
                       "basic_std_error": b.std_error, "variance_ratio_basic_over_equal": b.variance / e.variance,
-                      "reference_ratio_N62": 1.60}
+                      "reference_ratio_N62": 1.60, "gpus": 1}
     n, Nb = 4096, 24
     rng = np.random.default_rng(0)
     S0 = rng.uniform(50, 150, n); m = rng.uniform(0.8, 1.2, n); K = m * S0
@@ -304,7 +304,7 @@ def secondary_configs(dev):
     t = min(ms[1:])
     out["config5"] = {"workload": "4096 Asian calls, N=24, parameters from default_rng(0)",
                       "value": n * (1 << Nb) / (t * 1e-3), "unit": "paths/s", "kernel_ms": t,
-                      "value_option0": float(vals[0])}
+                      "value_option0": float(vals[0]), "gpus": 1}
     # K8 threshold-search engine: same exact values, leaves counted by binary
     # search (not visited) -> EFFECTIVE paths/s, a separate metric
     wl, classic_crr = workloads()
