@@ -185,11 +185,10 @@ static Layout choose_layout(const bp_tree* t, uint32_t payoffs, uint32_t flags, 
       if (((payoffs >> k) & 1) && !fast_kind_mask_supported(1u << k)) fast = false;
   }
   if (fast) {
-    std::vector<double> c, mx, mn, e;
-    std::vector<int> h;
-    build_inner(fast_L(), t->u, t->d, c, mx, mn, e, h);
-    for (double v : c)
-      if (!std::isfinite(v)) fast = false;
+    // every inner-table entry is a sum of L products of at most L factors u or
+    // d, so all are finite iff L * max(u, d, 1)^L is
+    const double big = std::max(1.0, std::max(t->u, t->d));
+    if (!std::isfinite(std::pow(big, fast_L()) * fast_L())) fast = false;
   }
   if (fast_possible) *fast_possible = fast;
   if (fast) {
