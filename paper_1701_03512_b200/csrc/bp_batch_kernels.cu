@@ -8,6 +8,7 @@
 // and then runs the same explicit leaf block as K1 (bp_leaf.cuh) over its
 // share of the option's thread prefixes, nodes in pairs.  Partials are
 // reduced in a fixed order (CTA tree, then ascending CTA index per option).
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include "bp_kernels.h"
@@ -23,7 +24,7 @@ constexpr int kBNP = 2;  // nodes per leaf block
 struct BatchArgs {
   int N;
   unsigned kind;
-  int cpo_log2;  // CTAs per option = 2^cpo_log2
+  BatchLayout lay;
 };
 
 template <unsigned KIND>
@@ -42,8 +43,13 @@ k_exact_batch(const BatchOption* __restrict__ opts, BatchArgs ba, double2* __res
   __shared__ double e_cls[NC], b_cls[NC];
   __shared__ double red_s[kBThreads], red_c[kBThreads];
 
-  const int opt = blockIdx.x >> ba.cpo_log2;
-  const int part = blockIdx.x & ((1 << ba.cpo_log2) - 1);
+  // CTA -> (option, part of 2^parts_log2): whole-layout options first, then the split tail
+  const long long head = (long long)ba.lay.n_whole << ba.lay.base_log2;
+  const bool in_head = (long long)blockIdx.x < head;
+  const int parts_log2 = in_head ? ba.lay.base_log2 : ba.lay.tail_log2;
+  const long long j = in_head ? (long long)blockIdx.x : (long long)blockIdx.x - head;
+  const int opt = (in_head ? 0 : ba.lay.n_whole) + (int)(j >> parts_log2);
+  const int part = (int)(j & ((1 << parts_log2) - 1));
   const BatchOption o = opts[opt];
   const int N = ba.N, D = N - kBL, Dp = D - kBM;
   const int tid = threadIdx.x;
@@ -121,7 +127,7 @@ k_exact_batch(const BatchOption* __restrict__ opts, BatchArgs ba, double2* __res
   const double INF = __longlong_as_double(0x7ff0000000000000ll);
   double ts = 0.0, tc = 0.0;
   const unsigned long long n_pre = 1ull << Dp;
-  const unsigned long long per = n_pre >> ba.cpo_log2;
+  const unsigned long long per = n_pre >> parts_log2;
   const unsigned long long p0 = (unsigned long long)part * per;
   const int zero = (N >> 10) & tid;  // 0, opaque to the compiler
   for (unsigned long long pi = p0 + tid; pi < p0 + per; pi += kBThreads) {
@@ -191,33 +197,58 @@ k_exact_batch(const BatchOption* __restrict__ opts, BatchArgs ba, double2* __res
   }
 }
 
-__global__ void k_batch_combine(const double2* __restrict__ partial, int n_opts, int cpo_log2, double* __restrict__ values) {
+__global__ void k_batch_combine(const double2* __restrict__ partial, BatchLayout lay, double* __restrict__ values) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n_opts) return;
+  if (i >= lay.n_opts) return;
+  const bool in_head = i < lay.n_whole;
+  const int parts_log2 = in_head ? lay.base_log2 : lay.tail_log2;
+  const long long first = in_head ? ((long long)i << lay.base_log2)
+                                  : ((long long)lay.n_whole << lay.base_log2) +
+                                        ((long long)(i - lay.n_whole) << lay.tail_log2);
   double s = 0.0, c = 0.0;
-  for (int k = 0; k < (1 << cpo_log2); ++k) {
-    const double2 p = partial[((long long)i << cpo_log2) + k];
+  for (int k = 0; k < (1 << parts_log2); ++k) {  // the option's parts in ascending order
+    const double2 p = partial[first + k];
     comp_merge(s, c, p.x, p.y);
   }
   values[i] = s + c;
 }
 
-int batch_ctas_per_option(int n_opts) {
+BatchLayout batch_layout(int n_opts, int N) {
   static const int forced = [] {
-    const char* e = std::getenv("BINPATHS_BATCH_CPO_LOG2");  // diagnostics
+    const char* e = std::getenv("BINPATHS_BATCH_CPO_LOG2");  // diagnostics: uniform CTAs per option
     return e ? std::atoi(e) : -1;
   }();
-  if (forced >= 0) return forced;
-  // enough CTAs to fill 148 SMs x 3 resident CTAs, at most 16 per option
-  int l = 0;
-  while (l < 4 && (long long)n_opts << l < 148 * 3) ++l;
-  return l;
+  const int max_log2 = std::min(4, N - 14);  // >= 1 thread prefix per CTA
+  int dev = 0, sms = 148, occ = 3;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long slots = (long long)sms * occ;  // resident CTAs (k_exact_batch: 3 per SM)
+  BatchLayout lay{n_opts, n_opts, 0, 0};
+  if (forced >= 0) {
+    lay.base_log2 = lay.tail_log2 = std::min(forced, max_log2);
+    return lay;
+  }
+  // few options: enough CTAs to fill the GPU, at most 16 per option
+  while (lay.base_log2 < max_log2 && ((long long)n_opts << lay.base_log2) < slots) ++lay.base_log2;
+  lay.tail_log2 = lay.base_log2;
+  if (lay.base_log2 == 0 && n_opts > slots) {
+    // whole waves of one CTA per option, then the remainder split so that its
+    // parts fill (at most) one wave of shorter CTAs
+    const int rem = (int)(n_opts % slots);
+    int t = 0;
+    while (t < max_log2 && ((long long)rem << (t + 1)) <= slots) ++t;
+    if (rem && t > 0) {
+      lay.n_whole = n_opts - rem;
+      lay.tail_log2 = t;
+    }
+  }
+  return lay;
 }
 
-cudaError_t launch_exact_batch(const BatchOption* opts_dev, int n_opts, int N, unsigned kind, double* values_dev,
-                               double2* scratch_dev, int cpo_log2, cudaStream_t st) {
-  BatchArgs ba{N, kind, cpo_log2};
-  const int grid = n_opts << cpo_log2;
+cudaError_t launch_exact_batch(const BatchOption* opts_dev, const BatchLayout& lay, int N, unsigned kind,
+                               double* values_dev, double2* scratch_dev, cudaStream_t st) {
+  BatchArgs ba{N, kind, lay};
+  const int grid = (int)lay.ctas();
 #define BP_B_CASE(K) \
   case K: k_exact_batch<K><<<grid, kBThreads, 0, st>>>(opts_dev, ba, scratch_dev); break;
   switch (kind) {
@@ -227,7 +258,7 @@ cudaError_t launch_exact_batch(const BatchOption* opts_dev, int n_opts, int N, u
 #undef BP_B_CASE
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  k_batch_combine<<<(n_opts + 255) / 256, 256, 0, st>>>(scratch_dev, n_opts, cpo_log2, values_dev);
+  k_batch_combine<<<(lay.n_opts + 255) / 256, 256, 0, st>>>(scratch_dev, lay, values_dev);
   return cudaGetLastError();
 }
 

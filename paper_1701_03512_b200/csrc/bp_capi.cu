@@ -1426,20 +1426,20 @@ extern "C" int bp_exact_batch(const bp_tree* trees, int n_opts, uint32_t payoff,
       cudaStreamDestroy(s);
     }
   } sg{st};
-  const int cpo = std::min(batch_ctas_per_option(n_opts), N - 14);  // >= 1 prefix per CTA
+  const BatchLayout blay = batch_layout(n_opts, N);
   DevBuf<BatchOption> d_o;
   DevBuf<double> d_v;
   DevBuf<double2> d_p;
   d_o.st = d_v.st = d_p.st = st;
   BP_CUDA(cudaMallocAsync((void**)&d_o.p, sizeof(BatchOption) * n_opts, st));
   BP_CUDA(cudaMallocAsync((void**)&d_v.p, sizeof(double) * n_opts, st));
-  BP_CUDA(cudaMallocAsync((void**)&d_p.p, sizeof(double2) * ((size_t)n_opts << cpo), st));
+  BP_CUDA(cudaMallocAsync((void**)&d_p.p, sizeof(double2) * (size_t)blay.ctas(), st));
   BP_CUDA(cudaMemcpyAsync(d_o.p, h.data(), sizeof(BatchOption) * n_opts, cudaMemcpyHostToDevice, st));
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0, st);
-  BP_CUDA(launch_exact_batch(d_o.p, n_opts, N, kind, d_v.p, d_p.p, cpo, st));
+  BP_CUDA(launch_exact_batch(d_o.p, blay, N, kind, d_v.p, d_p.p, st));
   cudaEventRecord(e1, st);
   BP_CUDA(cudaMemcpyAsync(values, d_v.p, sizeof(double) * n_opts, cudaMemcpyDeviceToHost, st));
   BP_CUDA(cudaStreamSynchronize(st));

@@ -25,9 +25,18 @@ cudaError_t launch_sb_reduce(const double2* unit_out, unsigned long long units_p
 struct BatchOption {
   double S0, K, u, d, p, disc;
 };
-cudaError_t launch_exact_batch(const BatchOption* opts_dev, int n_opts, int N, unsigned kind, double* values_dev,
-                               double2* scratch_dev, int cpo_log2, cudaStream_t st);
-int batch_ctas_per_option(int n_opts);  // log2 of CTAs per option
+// CTA layout of a batch: options [0, n_whole) get 2^base_log2 CTAs each, the
+// tail options [n_whole, n_opts) 2^tail_log2 each (the last wave's options are
+// split so it is not a mostly idle wave)
+struct BatchLayout {
+  int n_opts, n_whole, base_log2, tail_log2;
+  long long ctas() const {
+    return ((long long)n_whole << base_log2) + ((long long)(n_opts - n_whole) << tail_log2);
+  }
+};
+BatchLayout batch_layout(int n_opts, int N);
+cudaError_t launch_exact_batch(const BatchOption* opts_dev, const BatchLayout& lay, int N, unsigned kind,
+                               double* values_dev, double2* scratch_dev, cudaStream_t st);
 
 // Monte Carlo, see bp_mc_kernels.cu
 struct McArgs {
