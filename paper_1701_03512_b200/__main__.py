@@ -1,4 +1,7 @@
-"""python -m paper_1701_03512_b200 price|study|bench ... (reference __main__.py)."""
-from .cli import main_entry
+"""`python -m paper_1701_03512_b200 price|study|bench ...`: the GPU-backed CLI (cli.py)."""
+import sys
 
-main_entry()
+from .cli import main
+
+if __name__ == "__main__":
+    sys.exit(main())

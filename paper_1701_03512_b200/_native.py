@@ -24,19 +24,7 @@ FLAG_GENERIC = 2
 FLAG_NO_TIMING = 4
 FLAG_THRESHOLD = 8
 
-_STATUS = {
-    1: E.InvalidInput,
-    2: E.ProbabilityOutOfRange,
-    3: E.LengthMismatch,
-    4: E.InvalidWorkerCount,
-    5: E.RankOutOfRange,
-    6: E.PathDependentPayoff,
-    7: E.NonConstantProbs,
-    8: E.InfeasibleAllocation,
-    9: E.EnumerationGuard,
-    100: E.DeviceError,
-    101: E.DeviceError,
-}
+_STATUS = E.STATUS_CLASSES
 
 
 class BpTree(ctypes.Structure):
