@@ -559,6 +559,15 @@ struct bp_exact_plan {
   };
   Scratch scratch[64];
   std::mutex mu;
+  // captured enqueues of the class engine, keyed by (device, super-block
+  // range, output buffer, scratch): a repeated enqueue is one graph launch
+  struct Graph {
+    int dev, sb_first, sb_count;
+    double* out;
+    double2* scratch;
+    cudaGraphExec_t exec;
+  };
+  std::vector<Graph> graphs;
 };
 
 static int plan_build(const bp_tree* t, uint32_t payoffs, uint32_t flags, bp_exact_plan* P) {
@@ -828,18 +837,69 @@ extern "C" int bp_exact_plan_layout(const bp_exact_plan* plan, int* n_superblock
   return BP_OK;
 }
 
+static bool graphs_enabled();
+
+// The class-engine enqueue of a plan as a CUDA graph: the first enqueue for a
+// (device, range, output) runs the ordinary launches (which size the plan's
+// scratch); the second captures them on a private stream; later ones replay
+// the graph on the caller's stream -- one launch instead of K1 (12 KB of
+// arguments, ~11 us of host time) + K2.  Returns false to take the ordinary
+// path.
+static bool plan_enqueue_graph(bp_exact_plan* P, int dev, int sb_first, int sb_count, double* out_dev,
+                               cudaStream_t st) {
+  if (!graphs_enabled() || P->lay.engine != 1) return false;
+  double2* scratch;
+  {
+    std::lock_guard<std::mutex> g(P->mu);
+    scratch = P->scratch[dev].p;
+    const size_t need = sizeof(double2) * kNumKinds * (unsigned long long)sb_count * P->lay.units_per_sb;
+    if (!scratch || P->scratch[dev].bytes < need) return false;  // not sized yet: ordinary path first
+    for (auto& gr : P->graphs)
+      if (gr.dev == dev && gr.sb_first == sb_first && gr.sb_count == sb_count && gr.out == out_dev &&
+          gr.scratch == scratch)
+        return cudaGraphLaunch(gr.exec, st) == cudaSuccess;
+  }
+  for (auto& g : P->groups) cached_occupancy_fast(P->lay.L, g.km, false);  // no queries inside the capture
+  cudaStream_t cap;
+  if (cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking) != cudaSuccess) return false;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  bool ok = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+  if (ok) {
+    const int rc = plan_enqueue(P, dev, sb_first, sb_count, out_dev, nullptr, cap);
+    ok = cudaStreamEndCapture(cap, &graph) == cudaSuccess && rc == BP_OK && graph &&
+         cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess;
+  }
+  if (graph) cudaGraphDestroy(graph);
+  cudaStreamDestroy(cap);
+  if (!ok) {
+    cudaGetLastError();
+    return false;
+  }
+  {
+    std::lock_guard<std::mutex> g(P->mu);
+    P->graphs.push_back(bp_exact_plan::Graph{dev, sb_first, sb_count, out_dev, scratch, exec});
+  }
+  return cudaGraphLaunch(exec, st) == cudaSuccess;
+}
+
 extern "C" int bp_exact_plan_enqueue(bp_exact_plan* plan, int device, int sb_first, int sb_count, double* out_dev,
                                      uint64_t* hist_dev, void* stream) {
   if (!plan) return fail(BP_E_INVALID_INPUT, "plan is NULL");
   if (device < 0 || device >= bp_device_count()) return fail(BP_E_NO_DEVICE, "no CUDA device " + std::to_string(device));
   BP_CUDA(cudaSetDevice(device));
   keep_pool(device);
+  const bool cnt = (plan->flags & BP_FLAG_COUNT) != 0 || hist_dev;
+  if (!cnt && sb_first >= 0 && sb_count >= 1 && sb_first + sb_count <= plan->lay.n_sb &&
+      plan_enqueue_graph(plan, device, sb_first, sb_count, out_dev, static_cast<cudaStream_t>(stream)))
+    return BP_OK;
   return plan_enqueue(plan, device, sb_first, sb_count, out_dev, reinterpret_cast<unsigned long long*>(hist_dev),
                       static_cast<cudaStream_t>(stream));
 }
 
 extern "C" void bp_exact_plan_destroy(bp_exact_plan* plan) {
   if (!plan) return;
+  for (auto& g : plan->graphs) cudaGraphExecDestroy(g.exec);
   plan_release_scratch(plan, 0);
   delete plan;
 }
