@@ -60,3 +60,23 @@ def test_value_exact_distributed_world1(nccl_group):
     req = _req(26)
     got = bpd.value_exact_distributed(req, [bp.ASIAN_CALL], rank=0, world=1, device=0)
     assert got == bp.value_exact(req, devices=[0]).values
+
+
+def test_plan_enqueue_graph_replay_is_bitwise():
+    """The first enqueue of a plan runs the launches, the second captures
+    them as a graph, later ones replay it: all bitwise equal."""
+    import torch
+    from paper_1701_03512_b200.exact import tree_of
+    req = _req(28)
+    tree, keep = tree_of(req)
+    mask = (1 << 4) | (1 << 5)
+    sh = bpd.ShardedExact(tree, keep, mask, 0, 1, 0)
+    outs = []
+    for _ in range(4):
+        sh.local.zero_()
+        sh.enqueue()
+        torch.cuda.synchronize()
+        outs.append(bpd.combine(sh.local.cpu().numpy(), mask))
+    assert outs[0] == outs[1] == outs[2] == outs[3]
+    assert outs[0] == bp.value_exact(req, kinds=[bp.ASIAN_CALL, bp.FLOATING_LOOKBACK], devices=[0]).values
+    sh.close()
