@@ -29,7 +29,7 @@ import numpy as np
 
 from . import _native
 from .errors import InfeasibleAllocation, InvalidInput, InvalidWorkerCount
-from .paths import BernoulliPath, PathPartition, block_probability, make_partition
+from .paths import BernoulliPath, PathPartition, block_probability, make_partition, partition_masses
 from .payoffs import kind_bit
 
 
@@ -182,7 +182,7 @@ def allocate_strata(partition: PathPartition, params, R: int) -> list:
     """Largest-remainder split of R draws proportional to stratum mass,
     >= 1 draw for every positive-mass stratum, ties to the lower rank
     (mc.py:162-194)."""
-    masses = [block_probability(params, partition, m) for m in range(partition.m)]
+    masses = partition_masses(params, partition)
     positive = [m for m in range(partition.m) if masses[m] > 0.0]
     if R < len(positive):
         raise InfeasibleAllocation(f"R={R} draws cannot cover {len(positive)} strata with positive mass")
@@ -233,7 +233,7 @@ def _partitioned_reps(req, cfg, rep0, n_reps, stats=None):
     if cfg.R < cfg.M:
         raise InfeasibleAllocation(f"partitioned estimator needs R >= M, got R={cfg.R}, M={cfg.M}")
     part = _stratified_partition(req, cfg.M)
-    masses = [block_probability(req.params, part, m) for m in range(cfg.M)]
+    masses = partition_masses(req.params, part)
     alloc = allocate_strata(part, req.params, cfg.R)
     theta, sse, _ = (stats or _strata_stats)(req, part.prefix_width, alloc, cfg.seed, rep0, n_reps)
     return [_partitioned_from(req, cfg, masses, alloc, theta[k], sse[k], equal=False) for k in range(n_reps)]
@@ -241,7 +241,7 @@ def _partitioned_reps(req, cfg, rep0, n_reps, stats=None):
 
 def _equal_reps(req, cfg, rep0, n_reps, stats=None):
     part = _stratified_partition(req, cfg.M)
-    masses = [block_probability(req.params, part, m) for m in range(cfg.M)]
+    masses = partition_masses(req.params, part)
     alloc = [cfg.R] * cfg.M
     theta, sse, _ = (stats or _strata_stats)(req, part.prefix_width, alloc, cfg.seed, rep0, n_reps)
     return [_partitioned_from(req, cfg, masses, alloc, theta[k], sse[k], equal=True) for k in range(n_reps)]
@@ -251,7 +251,7 @@ def _shared_reps(req, cfg, rep0, n_reps):
     if cfg.R < 2:
         raise InvalidInput(f"shared estimator needs R >= 2, got {cfg.R}")
     part = _stratified_partition(req, cfg.M)
-    masses = np.array([block_probability(req.params, part, m) for m in range(cfg.M)])
+    masses = np.array(partition_masses(req.params, part))
     tree, keep = _tree(req)
     im = np.zeros(n_reps)
     isse = np.zeros(n_reps)

@@ -174,3 +174,14 @@ def test_mc_config_validation():
         bp.estimate_partitioned(req, bp.McConfig(R=64, M=3))
     with pytest.raises(bp.InvalidInput):
         bp.estimate_shared(req, bp.McConfig(R=1, M=2))
+
+
+def test_vectorised_partition_masses_are_bitwise_block_probability():
+    from paper_1701_03512_b200 import paths
+    rng = np.random.default_rng(3)
+    for N in (5, 12, 40):
+        P = bp.with_custom_probs(bp.MarketInputs(S0=1.0, K=1.0, q=0.0, sigma=0.2, T=1.0, N=N),
+                                 rng.uniform(0.05, 0.95, N))
+        for M in (1, 2, 3, 8, 16, 7):
+            part = bp.make_partition(N, M)
+            assert paths.partition_masses(P, part) == [bp.block_probability(P, part, m) for m in range(M)]
