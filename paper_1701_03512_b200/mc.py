@@ -186,10 +186,12 @@ def allocate_strata(partition: PathPartition, params, R: int) -> list:
     positive = [m for m in range(partition.m) if masses[m] > 0.0]
     if R < len(positive):
         raise InfeasibleAllocation(f"R={R} draws cannot cover {len(positive)} strata with positive mass")
-    targets = [R * w for w in masses]
-    alloc = [int(math.floor(t)) for t in targets]
-    order = sorted(range(partition.m), key=lambda m: (alloc[m] - targets[m], m))
-    for m in order[: R - sum(alloc)]:
+    targets = R * np.asarray(masses, dtype=np.float64)  # the same IEEE products as R * w per stratum
+    base = np.floor(targets)
+    # largest remainders first, ties to the lower stratum: primary key floor - target, then m
+    order = np.lexsort((np.arange(partition.m), base - targets))
+    alloc = [int(x) for x in base]
+    for m in order[: R - sum(alloc)].tolist():
         alloc[m] += 1
     floor_of = [1 if w > 0.0 else 0 for w in masses]
     while True:
