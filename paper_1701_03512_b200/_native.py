@@ -36,7 +36,7 @@ class BpTree(ctypes.Structure):
         ("u", ctypes.c_double),
         ("d", ctypes.c_double),
         ("disc", ctypes.c_double),
-        ("up_probs", ctypes.POINTER(ctypes.c_double)),
+        ("up_probs", ctypes.c_void_p),  # const double* (host); set from ndarray.ctypes.data
     ]
 
 
@@ -135,8 +135,10 @@ def u64ptr(a: np.ndarray):
 
 def make_tree(N, S0, K, u, d, disc, probs) -> tuple:
     """(BpTree, keep-alive array).  probs: per-step up probabilities."""
-    p = np.ascontiguousarray(np.broadcast_to(np.asarray(probs, dtype=np.float64), (N,)), dtype=np.float64)
-    t = BpTree(int(N), 0, float(S0), float(K), float(u), float(d), float(disc), dptr(p))
+    p = probs
+    if not (isinstance(p, np.ndarray) and p.dtype == np.float64 and p.shape == (N,) and p.flags.c_contiguous):
+        p = np.ascontiguousarray(np.broadcast_to(np.asarray(probs, dtype=np.float64), (N,)), dtype=np.float64)
+    t = BpTree(int(N), 0, float(S0), float(K), float(u), float(d), float(disc), p.ctypes.data)
     return t, p
 
 

@@ -191,8 +191,7 @@ def price_batch(N: int, S0, K, u, d, p, disc, kind, device: int = 0, with_time: 
     probs = np.ascontiguousarray(np.repeat(pa[:, None], N, axis=1))
     trees = (_native.BpTree * n)()
     for i in range(n):
-        trees[i] = _native.BpTree(int(N), 0, S0a[i], Ka[i], ua[i], da[i], da_[i],
-                                  probs[i].ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+        trees[i] = _native.BpTree(int(N), 0, S0a[i], Ka[i], ua[i], da[i], da_[i], probs[i].ctypes.data)
     out = np.zeros(n)
     ms = ctypes.c_double()
     _native.check(_native.lib().bp_exact_batch(trees, n, 1 << kind_bit(kind), int(device), _native.dptr(out),
