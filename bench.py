@@ -374,7 +374,10 @@ def run_ours(args):
     # configs[3] (stratified MC, N = 64) and configs[4] (batched exact) on rank 0's GPU
     extra45 = {}
     if rank == 0 and not args.no_config3:
-        extra45 = secondary_configs(dev)
+        try:  # secondary numbers must not cost the headline line
+            extra45 = secondary_configs(dev)
+        except Exception as exc:  # noqa: BLE001
+            extra45 = {"secondary_configs_error": f"{type(exc).__name__}: {exc}"}
 
     # e2e: the public API with host inputs and the result read back every step;
     # for N > 1 every rank takes part (value_exact_distributed: its shard + NCCL)
@@ -421,7 +424,10 @@ def run_ours(args):
            "d2h_bytes_per_step": 8 * 6 * 2 * sh.n_sb, "seconds_per_step": e2e_s,
            "path": e2e_path}
 
-    cpu = cpu_baseline(w, classic_crr) if world == 1 else None
+    try:
+        cpu = cpu_baseline(w, classic_crr) if world == 1 else None
+    except Exception as exc:  # noqa: BLE001
+        cpu = {"error": f"{type(exc).__name__}: {exc}"}
     launches_per_step = 2 * (1 if set(w["kinds"]) == {"asian-call", "float-lookback"} else len(w["kinds"]))
     line = {
         "metric": METRIC,
