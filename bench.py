@@ -11,7 +11,7 @@ floating lookback, K from default_rng(0)); config 3 (N = 36 Asian call) is
 measured in the same run and reported under "config3".
 
 N > 1 runs under torchrun, one rank per GPU; each rank owns a contiguous
-range of the 8 canonical super-blocks ("scaling": "weak" is NOT claimed --
+range of the 64 canonical super-blocks ("scaling": "weak" is NOT claimed --
 the total work is fixed, so scaling is "strong").
 
 --impl reference times the reference algorithm on the host CPU: the C

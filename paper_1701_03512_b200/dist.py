@@ -1,7 +1,7 @@
 """One process per GPU: shard the canonical super-blocks over ranks.
 
-The exact sum over 2^N paths splits into at most 8 canonical super-blocks
-(the top 3 bits of the node index, csrc/bp_exact.cuh).  Rank g of G owns a
+The exact sum over 2^N paths splits into at most 64 canonical super-blocks
+(the top 6 bits of the unit index, csrc/bp_exact.cuh).  Rank g of G owns a
 contiguous super-block range -- the paper's SPMD rank-prefix partition
 (paths.py:103-123 with r = log2 G).  Each rank enqueues its
 share on its own GPU (bp_exact_superblocks), the partials are exchanged with
