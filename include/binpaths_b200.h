@@ -107,12 +107,12 @@ typedef struct bp_exact_result {
 
 /* Exact expected value over all 2^N paths (value_exact_parallel).
  * payoffs: OR of bp_payoff bits.  devices: n_dev CUDA ordinals (n_dev >= 1);
- * the top log2(n_dev) super-block bits are sharded over them, one host
+ * contiguous ranges of the canonical super-blocks go to them, one host
  * thread per device.  The result is bitwise independent of n_dev.        */
 int bp_exact(const bp_tree* tree, uint32_t payoffs, uint32_t flags,
              int n_dev, const int* devices, bp_exact_result* out);
 
-/* Number of canonical super-blocks of a valuation (8 when 2^N is large).  */
+/* Number of canonical super-blocks of a valuation (64 when 2^N is large).  */
 int bp_exact_layout(const bp_tree* tree, uint32_t payoffs, uint32_t flags,
                     int* n_superblocks, int* engine, int* inner_bits);
 

@@ -8,7 +8,7 @@ share on its own GPU (bp_exact_superblocks), the partials are exchanged with
 ONE collective -- all_gather of a few hundred bytes over NCCL, the only
 cross-GPU step (the paper's MPI.Reduce) -- and every rank
 combines all partials in ascending super-block order, so the result is
-bitwise identical for G = 1, 2, 4, 8.
+bitwise identical for every G.
 
 torch.distributed is plumbing here (process group, device buffers, NCCL);
 the work is in the engine's kernels.  The combine logic is exercised on CPU
