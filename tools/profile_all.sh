@@ -3,7 +3,7 @@
 # without ncu and must exit 0; then the launch list of one bench run and one
 # ncu --set full capture per dominant kernel.  Output: gpurun_out/prof/.
 set -u
-O=gpurun_out/prof
+O=${1:-gpurun_out/prof}
 mkdir -p $O
 NCU="ncu --set full --clock-control none --import-source on"
 run() { echo "== $*" >> $O/runs.log; timeout 600 "$@" >> $O/runs.log 2>&1; echo "rc=$?" >> $O/runs.log; }
