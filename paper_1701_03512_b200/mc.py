@@ -29,7 +29,7 @@ import numpy as np
 
 from . import _native
 from .errors import InfeasibleAllocation, InvalidInput, InvalidWorkerCount
-from .paths import BernoulliPath, PathPartition, block_probability, make_partition, partition_masses
+from .paths import BernoulliPath, PathPartition, make_partition, partition_masses
 from .payoffs import kind_bit
 
 

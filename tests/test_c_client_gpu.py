@@ -1,7 +1,6 @@
 """The C ABI from plain C (examples/bp_price.c, built by build()): BASELINE
 configs[0] against the reference golden, leaf bookkeeping, and the status-code
 error path -- no Python between the caller and the engine."""
-import os
 import subprocess
 
 import pytest

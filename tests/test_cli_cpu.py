@@ -3,7 +3,6 @@
 not launch a kernel, and the bench rendering pinned to the reference's own
 output (tests/golden/cli_reference.json, tools/make_goldens.py cli)."""
 import json
-import os
 import subprocess
 import sys
 import time

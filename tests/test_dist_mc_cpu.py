@@ -12,7 +12,6 @@ the all_gather and the rank-order Chan merge are exercised without a GPU.
 import math
 import os
 import socket
-from types import SimpleNamespace
 
 import numpy as np
 import pytest

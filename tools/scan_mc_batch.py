@@ -1,5 +1,4 @@
 """Time BASELINE configs[3] (stratified MC, N=64) and configs[4] (batched exact, 4096 x N=24)."""
-import math
 import os
 import sys
 import time
