@@ -26,8 +26,9 @@
 //   class, sorted in the compare direction (host side, per tree), then cut
 //   into groups of <= kGroup positions.  Inside a group the in-the-money leaves
 //   are therefore a prefix: the per-leaf compares (DSETP + predicated
-//   increment) give the count n, and the group's contribution sum_ITM c_s
-//   is the precomputed prefix sum P_g[n] (one shared-memory load per group).
+//   increment, in independent chains of kChain leaves) give the count n, and
+//   the group's contribution sum_ITM c_s is the precomputed prefix sum P_g[n]
+//   (one shared-memory load per group).
 //   Per class the node keeps A_c = sum of ITM values and n_c = ITM count;
 //   the node value is sum_c w[h + c] (S A_c + base n_c), w[h] =
 //   e^{-qT} p^h (1-p)^{N-h} (exact.py:95,99 folded into one table).
@@ -72,10 +73,18 @@ __host__ __device__ constexpr int class_start(int L, int c) {
   for (int i = 0; i < c; ++i) s += binom(L, i);
   return s;
 }
+// Leaves per sorted group (prefix-sum lookup granularity) and leaves per
+// independent count chain inside a group: 32 / 4 measured best for K1 (both
+// the one- and two-table kernels) and K3 (profiles/r1_scan_group_chains*.log;
+// 8 / 8 before: 7 % slower).
 #ifndef BP_GROUP
-#define BP_GROUP 8
+#define BP_GROUP 32
 #endif
-constexpr int kGroup = BP_GROUP;  // leaves per sorted group (prefix-sum lookup granularity)
+constexpr int kGroup = BP_GROUP;
+#ifndef BP_CHAIN
+#define BP_CHAIN 4
+#endif
+constexpr int kChain = BP_CHAIN;
 __host__ __device__ constexpr int class_groups(int L, int c) { return (binom(L, c) + kGroup - 1) / kGroup; }
 __host__ __device__ constexpr int group_base(int L, int c) {
   int s = 0;

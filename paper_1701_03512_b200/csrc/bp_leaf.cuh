@@ -29,9 +29,15 @@ struct LeafGroups {
       if constexpr (kGroup * G < size) {
         constexpr int len = (size - kGroup * G) < kGroup ? (size - kGroup * G) : kGroup;
         constexpr int i0 = class_start(L, C) + kGroup * G;
-        int n[NP];
+        // the group's leaves count in independent chains of kChain (short
+        // dependency chains); the in-the-money leaves of the group are a
+        // prefix, so the sum of the chain counts indexes the group's prefix sums
+        constexpr int NCH = (len + kChain - 1) / kChain;
+        int nc[NP][NCH];
 #pragma unroll
-        for (int p = 0; p < NP; ++p) n[p] = 0;
+        for (int p = 0; p < NP; ++p)
+#pragma unroll
+          for (int c = 0; c < NCH; ++c) nc[p][c] = 0;
 #pragma unroll
         for (int j = 0; j < len; ++j) {
           // 16-byte loads of positions (2k, 2k+1) of this slot's table
@@ -39,7 +45,14 @@ struct LeafGroups {
           const double2 v = tb[i >> 1];
           const double x = (i & 1) ? v.y : v.x;
 #pragma unroll
-          for (int p = 0; p < NP; ++p) leaf_test<GT>(n[p], x, th[p]);
+          for (int p = 0; p < NP; ++p) leaf_test<GT>(nc[p][j / kChain], x, th[p]);
+        }
+        int n[NP];
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          n[p] = 0;
+#pragma unroll
+          for (int c = 0; c < NCH; ++c) n[p] += nc[p][c];
         }
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
