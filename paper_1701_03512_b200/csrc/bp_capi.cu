@@ -322,7 +322,7 @@ static int fill_fast_args(const bp_tree* t, const Layout& lay, unsigned km, std:
 
 // K1w arguments: per-step weights, one sorted table per kind + group prefix sums
 static int fill_w_args(const bp_tree* t, const Layout& lay, unsigned km, std::vector<unsigned char>& buf) {
-  constexpr int L = 8, NL = 1 << L, NG = NL / 8;
+  constexpr int L = 8, NL = 1 << L, NG = NL / kWGroup;
   buf.assign(sizeof(ExactWArgs<L>), 0);
   ExactWArgs<L>& a = *reinterpret_cast<ExactWArgs<L>*>(buf.data());
   const int N = t->n_steps, D = lay.D, m = lay.m, Dp = lay.Dp;
@@ -350,12 +350,12 @@ static int fill_w_args(const bp_tree* t, const Layout& lay, unsigned km, std::ve
     for (int i = 0; i < NL; ++i) a.tab[slot * NL + i] = v[ord[i]];
     for (int g = 0; g < NG; ++g) {
       double sa = 0.0, ca = 0.0, sb = 0.0, cb = 0.0;
-      a.gp[slot][g * 9] = make_double2(0.0, 0.0);
-      for (int n = 1; n <= 8; ++n) {
-        const int s2 = ord[8 * g + n - 1];
+      a.gp[slot][g * (kWGroup + 1)] = make_double2(0.0, 0.0);
+      for (int n = 1; n <= kWGroup; ++n) {
+        const int s2 = ord[kWGroup * g + n - 1];
         comp_add(sa, ca, w[s2] * v[s2]);
         comp_add(sb, cb, w[s2]);
-        a.gp[slot][g * 9 + n] = make_double2(sa + ca, sb + cb);
+        a.gp[slot][g * (kWGroup + 1) + n] = make_double2(sa + ca, sb + cb);
       }
     }
   }

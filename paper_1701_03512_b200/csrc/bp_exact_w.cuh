@@ -13,10 +13,14 @@ struct ExactWScalars {
   unsigned long long unit_first, unit_end;
 };
 
+// leaves per sorted group (one prefix-sum lookup) and per independent count
+// chain inside a group (as K1's kGroup / kChain; bp_exact.cuh)
+constexpr int kWGroup = 32, kWChain = 4;
+
 template <int L>
 struct __align__(16) ExactWArgs {
   double tab[2 << L];                  // per slot: inner values sorted in the compare direction
-  double2 gp[2][(1 << L) / 8 * 9];     // per slot, per group of 8: (sum w v, sum w) of the first n
+  double2 gp[2][(1 << L) / kWGroup * (kWGroup + 1)];  // per slot and group: (sum w v, sum w) of the first n
   double mid_c[kMidMax], mid_e[kMidMax], mid_mx[kMidMax], mid_mn[kMidMax], mid_w[kMidMax];
   double p[kMaxN], q[kMaxN];           // prefix steps: p_t and 1 - p_t
   ExactWScalars s;

@@ -33,23 +33,28 @@ __device__ __forceinline__ void wleaf_test(int& n, double x, double th) {
 template <int L, int NP, int SLOT, bool GT>
 __device__ __forceinline__ void wleaf_block(const double2* __restrict__ tb, const double2* __restrict__ gp,
                                             const double (&th)[NP], double (&A)[NP], double (&B)[NP]) {
-  constexpr int NG = (1 << L) / 8;
+  constexpr int NG = (1 << L) / kWGroup, NCH = kWGroup / kWChain;
 #pragma unroll
   for (int g = 0; g < NG; ++g) {
-    int n[NP];
+    int nc[NP][NCH];  // independent count chains; their sum is the group's ITM prefix length
 #pragma unroll
-    for (int p = 0; p < NP; ++p) n[p] = 0;
+    for (int p = 0; p < NP; ++p)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int i = SLOT * (1 << L) + 8 * g + j;
+      for (int c = 0; c < NCH; ++c) nc[p][c] = 0;
+#pragma unroll
+    for (int j = 0; j < kWGroup; ++j) {
+      const int i = SLOT * (1 << L) + kWGroup * g + j;
       const double2 v = tb[i >> 1];
       const double x = (i & 1) ? v.y : v.x;
 #pragma unroll
-      for (int p = 0; p < NP; ++p) wleaf_test<GT>(n[p], x, th[p]);
+      for (int p = 0; p < NP; ++p) wleaf_test<GT>(nc[p][j / kWChain], x, th[p]);
     }
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
-      const double2 q = gp[g * 9 + n[p]];  // (sum w v, sum w) of the group's first n entries
+      int n = 0;
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) n += nc[p][c];
+      const double2 q = gp[g * (kWGroup + 1) + n];  // (sum w v, sum w) of the group's first n entries
       A[p] += q.x;
       B[p] += q.y;
     }
@@ -93,9 +98,9 @@ k_exact_w(const __grid_constant__ ExactWArgs<L> a, double2* __restrict__ unit_ou
                 sFL = sAC + (int)kAC_;
   constexpr int NP = (NT == 2) ? 2 : 4;
 
-  __shared__ double2 sgp[NT][NG * 9];
+  __shared__ double2 sgp[NT][NG * (kWGroup + 1)];
   for (int t = 0; t < NT; ++t)
-    for (int i = threadIdx.x; i < NG * 9; i += blockDim.x) sgp[t][i] = a.gp[t][i];
+    for (int i = threadIdx.x; i < NG * (kWGroup + 1); i += blockDim.x) sgp[t][i] = a.gp[t][i];
   __syncthreads();
 
   const ExactWScalars& sc = a.s;
