@@ -122,6 +122,32 @@ class ShardedExact:
         return combine(src.detach().cpu().numpy(), self.mask)
 
 
+_SHARDED_LRU: "collections.OrderedDict" = None
+_SHARDED_CAP = 8
+
+
+def _sharded_for(tree, keep, mask: int, rank: int, world: int, device: int, group) -> ShardedExact:
+    """A cached ShardedExact per (contract, lattice, kinds, rank layout): a
+    repeated valuation reuses its prepared plan -- and, from the second call
+    on, the plan's captured CUDA graph."""
+    import collections
+
+    global _SHARDED_LRU
+    if _SHARDED_LRU is None:
+        _SHARDED_LRU = collections.OrderedDict()
+    key = (bytes(tree)[:48], np.asarray(keep).tobytes(), mask, rank, world, device, id(group))
+    sh = _SHARDED_LRU.get(key)
+    if sh is not None:
+        _SHARDED_LRU.move_to_end(key)
+        return sh
+    sh = ShardedExact(tree, keep, mask, rank, world, device)
+    _SHARDED_LRU[key] = sh
+    if len(_SHARDED_LRU) > _SHARDED_CAP:
+        _, old = _SHARDED_LRU.popitem(last=False)
+        old.close()
+    return sh
+
+
 def value_exact_distributed(req, kinds: Optional[Sequence] = None, rank: int = 0, world: int = 1,
                             device: int = 0, group=None) -> dict:
     """Exact values with this process as rank ``rank`` of ``world`` (one GPU each)."""
@@ -133,7 +159,7 @@ def value_exact_distributed(req, kinds: Optional[Sequence] = None, rank: int = 0
     for k in kinds:
         mask |= 1 << kind_bit(k)
     tree, keep = tree_of(req)
-    sh = ShardedExact(tree, keep, mask, rank, world, device)
+    sh = _sharded_for(tree, keep, mask, rank, world, device, group)
     sh.enqueue()
     sh.exchange(group)
     return sh.values()

@@ -58,8 +58,13 @@ def test_nccl_all_gather_and_combine_match_single_call(nccl_group):
 
 def test_value_exact_distributed_world1(nccl_group):
     req = _req(26)
-    got = bpd.value_exact_distributed(req, [bp.ASIAN_CALL], rank=0, world=1, device=0)
-    assert got == bp.value_exact(req, devices=[0]).values
+    want = bp.value_exact(req, devices=[0]).values
+    # repeated calls reuse the cached sharded plan (first launches, then its graph): all bitwise equal
+    for _ in range(3):
+        assert bpd.value_exact_distributed(req, [bp.ASIAN_CALL], rank=0, world=1, device=0) == want
+    other = _req(27)  # a different tree gets its own plan
+    assert bpd.value_exact_distributed(other, [bp.ASIAN_CALL], rank=0, world=1, device=0) == \
+        bp.value_exact(other, devices=[0]).values
 
 
 def test_plan_enqueue_graph_replay_is_bitwise():
