@@ -84,7 +84,10 @@ enum bp_status {
 typedef struct bp_tree {
     int32_t n_steps;          /* N, 1..62 (64 for bp_mc_*)                */
     int32_t reserved;
-    double S0;                /* > 0                                     */
+    double S0;                /* finite; bp_exact* also take S0 <= 0     *
+                               * (per-path walk, as the reference reads   *
+                               * S0 unchecked, exact.py:96,99); > 0 for   *
+                               * bp_mc_* and bp_exact_batch               */
     double K;                 /* strike                                  */
     double u;                 /* up factor   (> 0)                       */
     double d;                 /* down factor (> 0)                       */

@@ -113,8 +113,8 @@ def build_example() -> str:
 
 def build_variant(name: str, defines, parts=None, all_units: bool = False, sources=None) -> str:
     """Diagnostics: the library with extra -D flags on the K1 instantiation
-    parts (all parts, or the listed ones; every unit with all_units=True; the
-    units of the listed source basenames with sources=[...])
+    parts (all parts, or the listed ones) and on the units of the listed
+    source basenames (sources=[...]); every unit with all_units=True
     -> _lib/variants/<name>.so, for
     BINPATHS_LIB=... scans (tools/scan_variants.sh).  Other objects are
     shared with the main build."""
@@ -126,10 +126,10 @@ def build_variant(name: str, defines, parts=None, all_units: bool = False, sourc
     objs, procs = [], []
     for src, extra, obj in units():
         part = next((int(e.split("=")[1]) for e in extra if e.startswith("-DBP_FAST_PART=")), None)
-        if sources is not None:
-            chosen = os.path.basename(src) in sources
+        if part is not None:
+            chosen = all_units or parts is None or part in parts
         else:
-            chosen = all_units or (part is not None and (parts is None or part in parts))
+            chosen = all_units or (sources is not None and os.path.basename(src) in sources)
         if not chosen:
             objs.append(obj)
             continue

@@ -60,13 +60,16 @@ extern "C" int bp_device_count(void) {
 // validation (mirrors model.py:62-76 / exact.py:48-56 domains that the
 // engine itself relies on; the Python mirror validates request objects
 // before calling, so these are a second line of defence)
-static int validate_tree(const bp_tree* t, int max_n) {
+// any_sign_S0: the exact engine takes any finite S0, as the reference engine
+// reads inputs.S0 unchecked (exact.py:96,99) -- the sign-flip oracle route of
+// SURVEY 8(c); a non-positive S0 runs the per-path walk (choose_layout)
+static int validate_tree(const bp_tree* t, int max_n, bool any_sign_S0 = false) {
   if (!t) return fail(BP_E_INVALID_INPUT, "tree is NULL");
   if (t->n_steps < 1 || t->n_steps > max_n)
     return fail(BP_E_INVALID_INPUT, "N must be between 1 and " + std::to_string(max_n) + ", got " +
                                         std::to_string(t->n_steps));
-  if (!(t->S0 > 0.0) || !std::isfinite(t->S0))
-    return fail(BP_E_INVALID_INPUT, "S0 must be a positive finite number");
+  if (!std::isfinite(t->S0)) return fail(BP_E_INVALID_INPUT, "S0 must be finite");
+  if (!any_sign_S0 && !(t->S0 > 0.0)) return fail(BP_E_INVALID_INPUT, "S0 must be a positive finite number");
   if (!std::isfinite(t->K)) return fail(BP_E_INVALID_INPUT, "K must be finite");
   if (!(t->u > 0.0) || !std::isfinite(t->u) || !(t->d > 0.0) || !std::isfinite(t->d))
     return fail(BP_E_INVALID_INPUT, "u and d must be positive finite numbers");
@@ -135,7 +138,8 @@ static void build_inner(int L, double u, double d, std::vector<double>& c, std::
 static Layout choose_layout(const bp_tree* t, uint32_t payoffs, uint32_t flags, bool* fast_possible) {
   const int N = t->n_steps;
   Layout lay{};
-  if ((flags & BP_FLAG_THRESHOLD) && N >= kFastMinN && constant_p(t) && t->up_probs[0] > 0.0 &&
+  const bool pos = t->S0 > 0.0;  // the class engines divide by the node price
+  if ((flags & BP_FLAG_THRESHOLD) && pos && N >= kFastMinN && constant_p(t) && t->up_probs[0] > 0.0 &&
       t->up_probs[0] < 1.0 && t->u > t->d) {
     // K8 threshold search: 2^LT leaves per node, >= 2^16 nodes when N allows
     lay.engine = 2;
@@ -158,7 +162,9 @@ static Layout choose_layout(const bp_tree* t, uint32_t payoffs, uint32_t flags, 
   }();
   // K1w: per-leaf weights (any per-step probabilities) -- the explicit engine
   // for non-constant p, and for constant p when BINPATHS_WEIGHTED=1
-  if (!(flags & BP_FLAG_GENERIC) && N >= kFastMinN && t->u > t->d && (force_w || !constant_p(t))) {
+  // (leaf bookkeeping is not implemented in K1w: BP_FLAG_COUNT takes the path walk)
+  if (!(flags & (BP_FLAG_GENERIC | BP_FLAG_COUNT)) && pos && N >= kFastMinN && t->u > t->d &&
+      (force_w || !constant_p(t))) {
     lay.engine = 3;
     lay.L = 8;
     lay.D = N - lay.L;
@@ -174,7 +180,7 @@ static Layout choose_layout(const bp_tree* t, uint32_t payoffs, uint32_t flags, 
     if (fast_possible) *fast_possible = true;
     return lay;
   }
-  bool fast = !(flags & BP_FLAG_GENERIC) && N >= kFastMinN && constant_p(t);
+  bool fast = !(flags & BP_FLAG_GENERIC) && pos && N >= kFastMinN && constant_p(t);
   if (fast) {
     const double p = t->up_probs[0];
     if (!(p > 0.0 && p < 1.0)) fast = false;  // degenerate: single-path mass, walk it
@@ -200,7 +206,8 @@ static Layout choose_layout(const bp_tree* t, uint32_t payoffs, uint32_t flags, 
       const char* e = std::getenv("BINPATHS_UNIT_LOG2");
       return e ? std::atoi(e) : kUnitTargetLog2;
     }();
-    lay.m = std::max(1, std::min(6, free_bits - target));  // >= 1: nodes go in pairs
+    // n_mid = 2^m is a multiple of the nodes per leaf block
+    lay.m = std::max(std::max(1, kNodesPerBlockLog2), std::min(6, free_bits - target));
     lay.Dp = lay.D - lay.m;
     const int unit_bits = free_bits - lay.m;
     lay.q = std::max(0, unit_bits - 18);
@@ -816,7 +823,7 @@ static int enqueue_superblocks(const bp_tree* t, uint32_t payoffs, uint32_t flag
 }
 
 extern "C" int bp_exact_plan_create(const bp_tree* tree, uint32_t payoffs, uint32_t flags, bp_exact_plan** out) {
-  int rc = validate_tree(tree, 62);
+  int rc = validate_tree(tree, 62, true);
   if (rc) return rc;
   if ((rc = kinds_ok(payoffs))) return rc;
   if (!out) return fail(BP_E_INVALID_INPUT, "plan pointer is NULL");
@@ -906,7 +913,7 @@ extern "C" void bp_exact_plan_destroy(bp_exact_plan* plan) {
 
 extern "C" int bp_exact_layout(const bp_tree* tree, uint32_t payoffs, uint32_t flags, int* n_superblocks,
                                int* engine, int* inner_bits) {
-  int rc = validate_tree(tree, 62);
+  int rc = validate_tree(tree, 62, true);
   if (rc) return rc;
   if ((rc = kinds_ok(payoffs))) return rc;
   const Layout lay = choose_layout(tree, payoffs, flags, nullptr);
@@ -918,7 +925,7 @@ extern "C" int bp_exact_layout(const bp_tree* tree, uint32_t payoffs, uint32_t f
 
 extern "C" int bp_exact_superblocks(const bp_tree* tree, uint32_t payoffs, uint32_t flags, int device, int sb_first,
                                     int sb_count, double* out_dev, uint64_t* hist_dev, void* stream) {
-  int rc = validate_tree(tree, 62);
+  int rc = validate_tree(tree, 62, true);
   if (rc) return rc;
   if ((rc = kinds_ok(payoffs))) return rc;
   if (device < 0 || device >= bp_device_count()) return fail(BP_E_NO_DEVICE, "no CUDA device " + std::to_string(device));
@@ -1153,7 +1160,7 @@ static void run_device_job(const bp_tree* t, uint32_t payoffs, uint32_t flags, D
 
 extern "C" int bp_exact(const bp_tree* tree, uint32_t payoffs, uint32_t flags, int n_dev, const int* devices,
                         bp_exact_result* out) {
-  int rc = validate_tree(tree, 62);
+  int rc = validate_tree(tree, 62, true);
   if (rc) return rc;
   if ((rc = kinds_ok(payoffs))) return rc;
   if (!out) return fail(BP_E_INVALID_INPUT, "result pointer is NULL");

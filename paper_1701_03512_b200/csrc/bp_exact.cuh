@@ -94,6 +94,25 @@ __host__ __device__ constexpr int group_base(int L, int c) {
 __host__ __device__ constexpr int n_groups(int L) { return group_base(L, L + 1); }
 constexpr int kGroupSlots = kGroup + 1;  // prefix sums for n = 0..kGroup
 
+// K1 leaf-block configuration (shared by the kernels and the host layout):
+// BP_GRAY  -- leaf counts: 0 = predicated increments in chains of kChain,
+//             1 = Gray-code predicate chains (bp_gray.cuh);
+// BP_FOLD  -- 1 = each class folds into two per-node sums right after its
+//             groups (Gray mode only);
+// BP_NP    -- nodes per leaf block: every table load feeds NP compares.
+#ifndef BP_GRAY
+#define BP_GRAY 1
+#endif
+#ifndef BP_FOLD
+#define BP_FOLD 1
+#endif
+#ifndef BP_NP
+#define BP_NP 2
+#endif
+constexpr int kNodesPerBlock = BP_NP;
+constexpr int kNodesPerBlockLog2 = BP_NP == 4 ? 2 : BP_NP == 2 ? 1 : 0;
+static_assert(BP_NP == 1 || BP_NP == 2 || BP_NP == 4, "BP_NP must be 1, 2 or 4");
+
 template <int L>
 struct __align__(16) ExactArgs {
   // inner tables by position (class-major, sorted in the compare direction

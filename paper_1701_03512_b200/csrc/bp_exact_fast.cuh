@@ -7,9 +7,13 @@
 #include "bp_kernels.h"
 #include "bp_leaf.cuh"
 
+#if BP_FOLD && !BP_GRAY
+#error "BP_FOLD needs the Gray tables (BP_GRAY=1)"
+#endif
 #ifndef BP_TAB_SMEM
 #define BP_TAB_SMEM 0  // inner tables: 0 = constant bank (uniform LDCU), 1 = shared memory (LDS.128)
 #endif
+
 
 namespace bp {
 
@@ -19,8 +23,14 @@ namespace bp {
 __host__ __device__ constexpr int fast_tables(unsigned km) {
   return (int)((km >> kAC) & 1) + (int)((km >> kAP) & 1) + (int)((km >> kFL) & 1) + (int)((km >> kFLP) & 1);
 }
+#ifndef BP_MINB1
+#define BP_MINB1 3  // resident CTAs per SM targeted by the one-table kernels
+#endif
+#ifndef BP_MINB2
+#define BP_MINB2 2  // ... and by the fused two-table kernels
+#endif
 template <int L, unsigned KM, bool CNT>
-__global__ void __launch_bounds__(256, fast_tables(KM) == 2 ? 2 : 3)
+__global__ void __launch_bounds__(256, fast_tables(KM) == 2 ? BP_MINB2 : BP_MINB1)
 k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_out,
              unsigned long long* __restrict__ hist) {
   constexpr int NC = L + 1;
@@ -31,20 +41,49 @@ k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_
   // table slots in kind order AC, AP, FL, FLP
   constexpr int NT = (int)kAC_ + (int)kAP_ + (int)kFL_ + (int)kFLP_;
   static_assert(NT <= 2, "at most two tables per launch");
+  static_assert(!(kAC_ && kAP_), "the Asian call and put share one threshold slot order; launch them apart");
   constexpr int slotAC = 0, slotAP = (int)kAC_, slotFL = (int)kAC_ + (int)kAP_, slotFLP = slotFL + (int)kFL_;
   // nodes per leaf block: each table load feeds NP compares
-  constexpr int NP = 2;
+  constexpr int NP = kNodesPerBlock;
 
   __shared__ double sw[kMaxN + 2 + NC];
   __shared__ unsigned long long shist[kMaxN + 2];
+#if BP_GRAY
+  __shared__ __align__(16) double2 sgray[NT > 0 ? NT : 1][NG * kGraySlots];
+  for (int t = 0; t < NT; ++t)
+    for (int i = threadIdx.x; i < NG * kGraySlots; i += blockDim.x)
+      sgray[t][i] = gray_table_entry(&a.gpre[t][i / kGraySlots][0], (unsigned)(i % kGraySlots), BP_FOLD != 0);
+#define BP_GTAB(SLOT) reinterpret_cast<const char*>(&sgray[SLOT][0])
+#define BP_LEAF(SLOT, GTV, TH) leaf_block_gray<L, NP, SLOT, GTV>(tb, BP_GTAB(SLOT), TH, acc, cnt)
+#else
   __shared__ double sgpre[NT > 0 ? NT : 1][NG * kGroupSlots];
+  for (int t = 0; t < NT; ++t)
+    for (int i = threadIdx.x; i < NG * kGroupSlots; i += blockDim.x) sgpre[t][i] = (&a.gpre[t][0][0])[i];
+#define BP_LEAF(SLOT, GTV, TH) leaf_block<L, NP, SLOT, GTV>(tb, sgpre[SLOT], TH, acc, cnt)
+#endif
 #if BP_TAB_SMEM
   __shared__ __align__(16) double stab[NT > 0 ? NT << L : 2];
   for (int i = threadIdx.x; i < (NT << L); i += blockDim.x) stab[i] = a.tab[i];
 #endif
   for (int i = threadIdx.x; i < kMaxN + 2 + NC; i += blockDim.x) sw[i] = (i < kMaxN + 2) ? a.w[i] : 0.0;
-  for (int t = 0; t < NT; ++t)
-    for (int i = threadIdx.x; i < NG * kGroupSlots; i += blockDim.x) sgpre[t][i] = (&a.gpre[t][0][0])[i];
+#if BP_FOLD
+  // per node up count h: W1[h] = sum_c w[h+c] C(L,c), W2[h] = sum_c w[h+c] C(L,c) e_c (the lookback
+  // kinds' out-of-the-money and terminal terms), fixed order
+  constexpr bool needW = kFL_ || kFLP_;
+  __shared__ double sW1[needW ? kMaxN + 2 : 1], sW2[needW ? kMaxN + 2 : 1];
+  if (needW) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < kMaxN + 2; i += blockDim.x) {
+      double w1 = 0.0, w2 = 0.0;
+      for (int c = 0; c < NC; ++c) {
+        w1 = fma(sw[i + c], a.b_cls[c], w1);
+        w2 = fma(sw[i + c] * a.b_cls[c], a.e_cls[c], w2);
+      }
+      sW1[i] = w1;
+      sW2[i] = w2;
+    }
+  }
+#endif
   if (CNT)
     for (int i = threadIdx.x; i < kMaxN + 2; i += blockDim.x) shist[i] = 0ull;
   __syncthreads();
@@ -102,11 +141,44 @@ k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_
       // --- per kind: the leaf block (2^L explicit leaf tests per node), then
       // the class finalisation, node value = sum_c w[h+c] * contrib_c.  Kinds
       // run one after the other so only one kind's accumulators are live.
+#if BP_FOLD
+      // node value, affine in sA = sum_c w[h+c] A_c and sN = sum_c w[h+c] n_c
+      // (A_c / n_c: class-c in-the-money table sum and count):
+      //   AC  S sA + base sN              AP  -(S sA + base sN)
+      //   FL  S (sA - W2) + Mx (W1 - sN)  FLP K sN - S sA + max(K - Mn, 0) (W1 - sN)
+      if (kAC_ || kAP_) {
+        double sA[NP], sN[NP];
+        if (kAC_) leaf_block_fold<L, NP, slotAC, true>(tb, BP_GTAB(slotAC), sw, hn, thC, sA, sN);
+        else leaf_block_fold<L, NP, slotAP, false>(tb, BP_GTAB(slotAP), sw, hn, thC, sA, sN);
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          const double v = fma(Sn[p], sA[p], base[p] * sN[p]);
+          if (kAC_) comp_add(ts[kAC], tc[kAC], v);
+          else comp_add(ts[kAP], tc[kAP], -v);
+        }
+      }
+      if (kFL_) {
+        double sA[NP], sN[NP];
+        leaf_block_fold<L, NP, slotFL, true>(tb, BP_GTAB(slotFL), sw, hn, thX, sA, sN);
+#pragma unroll
+        for (int p = 0; p < NP; ++p)
+          comp_add(ts[kFL], tc[kFL], fma(Sn[p], sA[p] - sW2[hn[p]], Mxn[p] * (sW1[hn[p]] - sN[p])));
+      }
+      if (kFLP_) {
+        double sA[NP], sN[NP];
+        leaf_block_fold<L, NP, slotFLP, false>(tb, BP_GTAB(slotFLP), sw, hn, thN, sA, sN);
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          const double flat = fmax(sc.K - Mnn[p], 0.0);
+          comp_add(ts[kFLP], tc[kFLP], fma(flat, sW1[hn[p]] - sN[p], fma(sc.K, sN[p], -Sn[p] * sA[p])));
+        }
+      }
+#else
       if (kAC_) {
         double acc[NP][NC];
         int cnt[NP][NC];
         zero_acc<NP, NC>(acc, cnt);
-        leaf_block<L, NP, slotAC, true>(tb, sgpre[slotAC], thC, acc, cnt);
+        BP_LEAF(slotAC, true, thC);
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
           double v = 0.0;
@@ -119,7 +191,7 @@ k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_
         double acc[NP][NC];
         int cnt[NP][NC];
         zero_acc<NP, NC>(acc, cnt);
-        leaf_block<L, NP, slotAP, false>(tb, sgpre[slotAP], thC, acc, cnt);
+        BP_LEAF(slotAP, false, thC);
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
           double v = 0.0;
@@ -132,7 +204,7 @@ k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_
         double acc[NP][NC];
         int cnt[NP][NC];
         zero_acc<NP, NC>(acc, cnt);
-        leaf_block<L, NP, slotFL, true>(tb, sgpre[slotFL], thX, acc, cnt);
+        BP_LEAF(slotFL, true, thX);
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
           double v = 0.0;
@@ -150,7 +222,7 @@ k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_
         double acc[NP][NC];
         int cnt[NP][NC];
         zero_acc<NP, NC>(acc, cnt);
-        leaf_block<L, NP, slotFLP, false>(tb, sgpre[slotFLP], thN, acc, cnt);
+        BP_LEAF(slotFLP, false, thN);
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
           double v = 0.0;
@@ -164,6 +236,7 @@ k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_
           comp_add(ts[kFLP], tc[kFLP], v);
         }
       }
+#endif
       if (kEC_ || kEP_) {
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
@@ -210,6 +283,9 @@ k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_
       if (shist[i]) atomicAdd(&hist[i], shist[i]);
   }
 }
+
+#undef BP_LEAF
+#undef BP_GTAB
 
 // launch wrappers
 template <int L, unsigned KM>

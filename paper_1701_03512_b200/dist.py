@@ -38,35 +38,45 @@ def shard_range(n_sb: int, rank: int, world: int) -> tuple:
     return first, base + (1 if rank < extra else 0)
 
 
+def shard_rows(n_sb: int, world: int) -> int:
+    """Rows of every rank's exchange buffer: the largest shard, so the
+    all_gather has equal counts for any world size (64 super-blocks over 3
+    ranks: 22 / 21 / 21 real rows, all padded to 22)."""
+    return -(-n_sb // world)
+
+
 def combine(partials: np.ndarray, mask: int) -> dict:
-    """Fixed-order (ascending super-block) compensated sum -> {tag: value}."""
+    """Fixed-order (ascending super-block) compensated sum -> {tag: value},
+    in the engine's host combine (bp_combine_superblocks); raises DeviceError
+    when the engine library is missing (no Python fallback)."""
     p = np.ascontiguousarray(partials, dtype=np.float64).reshape(-1, N_PAYOFFS, 2)
     vals = np.zeros(N_PAYOFFS)
-    if _native.available():
-        _native.check(_native.lib().bp_combine_superblocks(_native.dptr(p), p.shape[0], mask, _native.dptr(vals)))
-    else:  # the same TwoSum merge in Python (host logic tests without the .so)
-        for k in range(N_PAYOFFS):
-            if not (mask >> k) & 1:
-                continue
-            s = c = 0.0
-            for b in range(p.shape[0]):
-                s2, c2 = float(p[b, k, 0]), float(p[b, k, 1])
-                t = s + s2
-                bp = t - s
-                e = (s - (t - bp)) + (s2 - bp)
-                s, c = t, c + (c2 + e)
-            vals[k] = s + c
+    _native.check(_native.lib().bp_combine_superblocks(_native.dptr(p), p.shape[0], mask, _native.dptr(vals)))
     return {BIT_TAG[k]: float(vals[k]) for k in range(N_PAYOFFS) if (mask >> k) & 1}
 
 
-def gather_partials(local, world: int, group=None):
-    """all_gather of each rank's [count, 6, 2] partial tensor (equal counts)."""
+def gather_partials(local, n_sb: int, world: int, group=None):
+    """all_gather of every rank's padded [shard_rows, 6, 2] partials (equal
+    counts for any world size) -> [world * shard_rows, 6, 2]; unpad() keeps
+    the real rows."""
     import torch
     import torch.distributed as dist
 
-    out = torch.empty((world * local.shape[0],) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    per = local.shape[0]
+    if per != shard_rows(n_sb, world):
+        raise ValueError(f"exchange buffer has {per} rows, expected {shard_rows(n_sb, world)}")
+    out = torch.empty((world * per,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
     dist.all_gather_into_tensor(out, local.contiguous(), group=group)
     return out
+
+
+def unpad(gathered, n_sb: int, world: int):
+    """The real rows of a gathered exchange buffer in rank order = ascending
+    super-block order (rank g's rows are super-blocks shard_range(n_sb, g));
+    numpy arrays and tensors alike."""
+    per = shard_rows(n_sb, world)
+    idx = np.concatenate([np.arange(g * per, g * per + shard_range(n_sb, g, world)[1]) for g in range(world)])
+    return gathered[idx]
 
 
 class ShardedExact:
@@ -89,7 +99,9 @@ class ShardedExact:
                                                          ctypes.byref(L)))
         self.n_sb, self.engine, self.inner_bits = n_sb.value, eng.value, L.value
         self.first, self.count = shard_range(self.n_sb, rank, world)
-        self.local = torch.zeros((self.count, N_PAYOFFS, 2), dtype=torch.float64, device=f"cuda:{device}")
+        # padded to the largest shard: equal all_gather counts for any world size
+        self.local = torch.zeros((shard_rows(self.n_sb, world), N_PAYOFFS, 2), dtype=torch.float64,
+                                 device=f"cuda:{device}")
         self.gathered = None
 
     def enqueue(self, stream=None):
@@ -114,12 +126,14 @@ class ShardedExact:
             pass
 
     def exchange(self, group=None):
-        self.gathered = gather_partials(self.local, self.world, group) if self.world > 1 else self.local
+        self.gathered = (gather_partials(self.local, self.n_sb, self.world, group) if self.world > 1
+                         else self.local[:self.count])
         return self.gathered
 
     def values(self) -> dict:
-        src = self.gathered if self.gathered is not None else self.local
-        return combine(src.detach().cpu().numpy(), self.mask)
+        if self.gathered is None or self.world == 1:
+            return combine(self.local[:self.count].detach().cpu().numpy(), self.mask)
+        return combine(unpad(self.gathered.detach().cpu().numpy(), self.n_sb, self.world), self.mask)
 
 
 _SHARDED_LRU: "collections.OrderedDict" = None

@@ -96,8 +96,8 @@ def tree_of(req):
     if probs.shape != (N,):
         raise LengthMismatch(f"tree has {probs.shape[0]} steps but inputs say N={N}")
     S0 = float(inp.S0)
-    if not (S0 > 0.0 and math.isfinite(S0)):
-        raise InvalidInput(f"S0 must be a positive finite number, got {S0}")
+    if not math.isfinite(S0):  # any sign: the reference engine reads S0 unchecked (exact.py:96,99)
+        raise InvalidInput(f"S0 must be a finite number, got {S0}")
     disc = math.exp(-float(inp.q) * float(inp.T))
     return _native.make_tree(N, S0, float(inp.K), float(par.u), float(par.d), disc, probs)
 

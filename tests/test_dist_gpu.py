@@ -49,9 +49,9 @@ def test_nccl_all_gather_and_combine_match_single_call(nccl_group):
     tree, keep = tree_of(req)
     sh = bpd.ShardedExact(tree, keep, (1 << 4) | (1 << 5), 0, 1, 0)
     sh.enqueue()
-    gathered = bpd.gather_partials(sh.local, 1)  # the NCCL collective itself
+    gathered = bpd.gather_partials(sh.local, sh.n_sb, 1)  # the NCCL collective itself
     torch.cuda.synchronize()
-    got = bpd.combine(gathered.cpu().numpy(), (1 << 4) | (1 << 5))
+    got = bpd.combine(bpd.unpad(gathered.cpu().numpy(), sh.n_sb, 1), (1 << 4) | (1 << 5))
     assert got == want  # bitwise: same canonical super-blocks, same fixed-order combine
     sh.close()
 
