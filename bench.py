@@ -10,14 +10,16 @@ combined.  Default workload = BASELINE configs[1] (N = 30, Asian call +
 floating lookback, K from default_rng(0)); config 3 (N = 36 Asian call) is
 measured in the same run and reported under "config3".
 
-N > 1 runs under torchrun, one rank per GPU; each rank owns a contiguous
-range of the 64 canonical super-blocks ("scaling": "weak" is NOT claimed --
-the total work is fixed, so scaling is "strong").
+--gpus N > 1 re-executes itself under torchrun with N ranks, one per GPU
+(paper_1701_03512_b200.launch); fewer than N visible GPUs is an error, never
+a silent one-GPU run.  Each rank owns a contiguous range of the 64 canonical
+super-blocks; the total 2^N work is fixed, so "scaling" is "strong".
 
 --impl reference times the reference algorithm on the host CPU: the C
-restatement in oracle/ (the reference is pure Python and cannot be compiled;
-its own numpy engine was measured at 1.3e7 paths/s on 8 cores, BASELINE.md
-§3), on a bounded sample of the same workload with every host thread.
+restatement in oracle/ (the reference is pure Python and cannot be compiled)
+on every host thread, whole valuations per step when they fit the run's
+time budget.  The stock reference package (baseline/_ref, numpy) is timed
+beside it at N = 24 as a labelled second baseline.
 """
 from __future__ import annotations
 
@@ -37,6 +39,9 @@ sys.path.insert(0, ROOT)
 W_OPS = {"asian-call": 3, "float-lookback": 3}  # FP64-pipe ops per path per payoff
 # one metric string for both arms (ours and --impl reference)
 METRIC = "exact-enumeration paths/sec (N=30 two payoffs in one pass; N=36 under config3)"
+FP64_LANES_PER_SM = 64   # B200: 64 FP64 lanes per SM per clock
+FP32_LANES_PER_SM = 128
+REF_BUDGET_S = 240.0     # the reference arm's whole run (all steps) stays within this
 
 
 def workloads():
@@ -52,7 +57,7 @@ def workloads():
 
 
 def workload_config(name, w):
-    """The workload keys both arms report (same config for the driver's ratio)."""
+    """The workload keys both arms report (identical config for the driver's ratio)."""
     return {"workload": name, "N": w["N"], "payoffs": w["kinds"], "K": w["K"], "S0": w["S0"], "r": w["r"],
             "sigma": w["sigma"], "T": w["T"]}
 
@@ -63,6 +68,16 @@ def make_req(w, classic_crr):
     inputs = bp.MarketInputs(S0=w["S0"], K=w["K"], q=w["r"], sigma=w["sigma"], T=w["T"], N=w["N"])
     kinds = [bp.resolve_kind(k) for k in w["kinds"]]
     return bp.ValuationRequest(inputs=inputs, params=P, kind=kinds[0], force_large=True), kinds, P
+
+
+def load_counters(workload):
+    """Per-launch counters of the dominant kernel from the committed ncu
+    capture of this instantiation (profiles/r2_kernel_counters.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r2_kernel_counters.json")) as f:
+            return json.load(f)[workload]
+    except Exception:  # noqa: BLE001
+        return None
 
 
 # ---------------------------------------------------------------------------
@@ -121,20 +136,24 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
+# CPU baselines (the only place bench.py runs oracle/ or the stock reference)
+def _oracle_paths(w, classic_crr, n, threads):
+    import oracle
+    P = classic_crr(w["N"], w["sigma"], w["r"], w["T"])
+    disc = math.exp(-w["r"] * w["T"])
+    t0 = time.perf_counter()
+    vals, paths = oracle.exact_range(w["N"], w["S0"], w["K"], P.u, P.d, P.up_probs[0], disc, w["kinds"], 0, n,
+                                     threads)
+    return paths, time.perf_counter() - t0, vals
+
+
 def cpu_baseline(w, classic_crr, budget_s=12.0):
     """Reference algorithm (oracle/ C restatement) on every host thread, on a
     bounded contiguous sample of the workload's path codes."""
-    import oracle
-    P = classic_crr(w["N"], w["sigma"], w["r"], w["T"])
     threads = os.cpu_count() or 1
-    disc = math.exp(-w["r"] * w["T"])
     n = 1 << 16
-    elapsed = 0.0
     while True:
-        t0 = time.perf_counter()
-        _, paths = oracle.exact_range(w["N"], w["S0"], w["K"], P.u, P.d, P.up_probs[0], disc, w["kinds"], 0, n,
-                                      threads)
-        elapsed = time.perf_counter() - t0
+        paths, elapsed, _ = _oracle_paths(w, classic_crr, n, threads)
         if elapsed * 4 > budget_s or n >= (1 << w["N"]):
             break
         n <<= 2
@@ -143,34 +162,107 @@ def cpu_baseline(w, classic_crr, budget_s=12.0):
                       f"{elapsed:.2f} s wall, oracle/bp_oracle.c (per-path walk as exact.py:83-100)"}
 
 
+def stock_reference_baseline(N=24):
+    """The UNMODIFIED reference package (baseline/_ref, numpy) on this host:
+    value_exact_parallel(workers=os.cpu_count()) on config 2's lattice at
+    N = 24.  It has no Asian call / floating lookback
+    built-in: Asian call = ASIAN_PUT at (-S0, -K) (bit-identical to the
+    callable route), floating lookback = FIXED_LOOKBACK_PUT(-S0, 0) -
+    EUROPEAN_CALL(S0, 0); the three engine walls are summed."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "binpaths")):
+        return {"unavailable": "baseline/_ref not installed (see DESIGN.md)"}
+    sys.path.insert(0, ref)
+    try:
+        from types import SimpleNamespace
+
+        import numpy as np
+        import binpaths as B
+        wl, _ = workloads()
+        w = wl["config2"]
+        S0, K, r, sigma, T = w["S0"], w["K"], w["r"], w["sigma"], w["T"]
+        dt = T / N
+        u = math.exp(sigma * math.sqrt(dt))
+        d = 1 / u
+        p = (math.exp(r * dt) - d) / (u - d)
+        P = B.TreeParams(dt=dt, u=u, d=d, beta=0.5 * (u + d), up_probs=np.full(N, p))
+        cores = os.cpu_count() or 1
+
+        def run(kind, s0, k):
+            req = B.ValuationRequest(inputs=SimpleNamespace(S0=s0, K=k, q=r, T=T, N=N), params=P, kind=kind,
+                                     workers=cores, force_large=True)
+            t0 = time.perf_counter()
+            v = B.value_exact_parallel(req)
+            return v, time.perf_counter() - t0
+
+        ac, t1 = run(B.PayoffKind.ASIAN_PUT, -S0, -K)
+        flp, t2 = run(B.PayoffKind.FIXED_LOOKBACK_PUT, -S0, 0.0)
+        ec, t3 = run(B.PayoffKind.EUROPEAN_CALL, S0, 0.0)
+        wall = t1 + t2 + t3
+        return {"value": (1 << N) / wall, "unit": "paths/s", "cores": cores, "kind": "reference",
+                "sample": f"stock binpaths {getattr(B, '__version__', '0.1.0')} (baseline/_ref), "
+                          f"value_exact_parallel(workers={cores}), config-2 lattice at N={N}: Asian call by the "
+                          f"sign-flip route + floating lookback as two runs, 3 engine walls summed = {wall:.2f} s",
+                "values": {"asian-call": ac, "float-lookback": flp - ec}}
+    except Exception as exc:  # noqa: BLE001
+        return {"unavailable": f"{type(exc).__name__}: {exc}"}
+    finally:
+        sys.path.remove(ref)
+
+
 def run_reference(args):
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
+    """The reference arm: rank 0 only (other torchrun ranks exit 0)."""
+    if int(os.environ.get("RANK", "0")) != 0:
         return 0
     wl, classic_crr = workloads()
     w = wl[args.workload]
-    steps = []
+    threads = os.cpu_count() or 1
+    full = 1 << w["N"]
+    # size each step so the whole run stays within the budget: whole
+    # valuations when they fit, else the largest power-of-two code prefix
+    cal_n = min(full, 1 << 22)
+    _, cal_t, _ = _oracle_paths(w, classic_crr, cal_n, threads)
+    per_path = cal_t / cal_n
+    n = full
+    while n > cal_n and per_path * n * (args.steps + args.warmup) > REF_BUDGET_S:
+        n >>= 1
+    ts, paths = [], 0
     for i in range(args.warmup + args.steps):
-        cb = cpu_baseline(w, classic_crr, budget_s=4.0 if i >= args.warmup else 1.0)
+        p, t, vals = _oracle_paths(w, classic_crr, n, threads)
         if i >= args.warmup:
-            steps.append(cb)
-    v = statistics.median(s["value"] for s in steps)
-    total = 1 << w["N"]
+            ts.append(t)
+            paths = p
+    sec = sum(ts) / len(ts)
+    v = paths / sec
+    sample = (f"{'whole valuation' if n == full else 'code prefix'}: {paths} of 2^{w['N']} paths per step "
+              f"(codes [0, {paths})), {'+'.join(w['kinds'])} in one pass, {sec:.2f} s per step, "
+              f"oracle/bp_oracle.c (per-path walk as exact.py:83-100) on {threads} threads")
     line = {"metric": METRIC, "value": v, "unit": "paths/s",
-            "n_gpus": 0, "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / v * 1e3,
+            "n_gpus": 0, "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "impl": "reference",
-            "config": {**workload_config(args.workload, w), "parallelism": f"{os.cpu_count()} host threads"},
-            "cpu_baseline": {**steps[-1], "value": v},
+            "data": "synthetic (BASELINE configs; tree parameters, no dataset)", "impl": "reference",
+            "config": workload_config(args.workload, w),
+            "impl_detail": {"parallelism": f"{threads} host threads", "whole_valuation_per_step": n == full},
+            "cpu_baseline": {"value": v, "unit": "paths/s", "cores": threads, "kind": "port", "sample": sample},
             "e2e": {"value": v, "unit": "paths/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if n == full:
+        line["values"] = vals
+    if not args.no_stock:
+        line["stock_reference"] = stock_reference_baseline()
     print(json.dumps(line), flush=True)
     return 0
 
 
 # ---------------------------------------------------------------------------
+def _events(torch):
+    return torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+
 def time_workload(w, classic_crr, steps, warmup, rank, world, dev, group):
     """Device-timed steps (CUDA events on the launch stream), L2 flushed
-    between steps; returns (ms list, values, sharder)."""
+    between steps.  A step = this rank's super-blocks (K1 + K2) and, for
+    N > 1, the all_gather.  Also times the two halves alone: the rank's
+    kernels (its roofline) and the exchange (the fixed multi-GPU cost)."""
     import torch
     import torch.distributed as dist
     from paper_1701_03512_b200 import dist as bpd
@@ -189,21 +281,57 @@ def time_workload(w, classic_crr, steps, warmup, rank, world, dev, group):
         sh.enqueue(st)
         sh.exchange(group)
     torch.cuda.synchronize(dev)
-    times = []
-    for _ in range(steps):
-        flush.fill_(1)
-        if world > 1:
-            dist.barrier(group=group)
-        torch.cuda.synchronize(dev)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(st)
+
+    def timed(fn, n):
+        out = []
+        for _ in range(n):
+            flush.fill_(1)
+            if world > 1:
+                dist.barrier(group=group)
+            torch.cuda.synchronize(dev)
+            e0, e1 = _events(torch)
+            e0.record(st)
+            fn()
+            e1.record(st)
+            torch.cuda.synchronize(dev)
+            out.append(e0.elapsed_time(e1))
+        return out
+
+    def step():
         sh.enqueue(st)
         sh.exchange(group)
-        e1.record(st)
-        torch.cuda.synchronize(dev)
-        times.append(e0.elapsed_time(e1))
+
+    times = timed(step, steps)
     vals = sh.values()
-    return times, vals, sh, req, kinds
+    detail = {}
+    kern = timed(lambda: sh.enqueue(st), max(3, min(steps, 10)))
+    detail["kernel_ms"] = sum(kern) / len(kern)
+    if world > 1:
+        xch = timed(lambda: sh.exchange(group), max(3, min(steps, 10)))
+        detail["exchange_ms"] = sum(xch) / len(xch)
+    detail["superblocks"] = (sh.first, sh.count, sh.n_sb)
+    return times, vals, sh, req, kinds, detail
+
+
+def _max_over_ranks(x, world, dev):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{dev}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _gather_ranks(x, world, dev):
+    if world == 1:
+        return [x]
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{dev}")
+    out = torch.empty(world, dtype=torch.float64, device=f"cuda:{dev}")
+    dist.all_gather_into_tensor(out, t)
+    return [float(v) for v in out.cpu()]
 
 
 def e2e_seconds(bp, req, kinds, args, warmup, rank, world, dev, group):
@@ -211,7 +339,6 @@ def e2e_seconds(bp, req, kinds, args, warmup, rank, world, dev, group):
     Python floats out), max over ranks.  N = 1: value_exact (C ABI, one
     synchronous call); N > 1: value_exact_distributed on every rank (this
     rank's super-blocks, the NCCL all_gather, the host combine)."""
-    import torch
     import torch.distributed as dist
     from paper_1701_03512_b200 import dist as bpd
 
@@ -227,40 +354,64 @@ def e2e_seconds(bp, req, kinds, args, warmup, rank, world, dev, group):
         dt = time.perf_counter() - t0
         if i >= warmup:
             ts.append(dt)
-    med = statistics.median(ts)
+    med = _max_over_ranks(statistics.median(ts), world, dev)
     if world > 1:
-        t = torch.tensor([med], dtype=torch.float64, device=f"cuda:{dev}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
-        med = float(t.item())
         return med, "paper_1701_03512_b200.dist.value_exact_distributed(req, kinds, rank, world) on every rank"
     return med, "paper_1701_03512_b200.value_exact(req, kinds) -> bp_exact (C ABI)"
 
 
-def kernel_share(w, classic_crr, dev, reps=5):
-    """Duration of the dominant kernel alone (the leaf kernel + its reduce are
-    what one super-block launch enqueues) for the roofline line."""
-    import torch
-    from paper_1701_03512_b200 import dist as bpd
-    from paper_1701_03512_b200.exact import tree_of
-    from paper_1701_03512_b200.payoffs import kind_bit
-    req, kinds, P = make_req(w, classic_crr)
-    tree, keep = tree_of(req)
-    mask = 0
-    for k in kinds:
-        mask |= 1 << kind_bit(k)
-    sh = bpd.ShardedExact(tree, keep, mask, 0, 1, dev)
-    st = torch.cuda.current_stream(dev)
-    sh.enqueue(st)
-    torch.cuda.synchronize(dev)
-    ts = []
-    for _ in range(reps):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(st)
-        sh.enqueue(st)
-        e1.record(st)
-        torch.cuda.synchronize(dev)
-        ts.append(e0.elapsed_time(e1))
-    return min(ts)
+def fp64_peak(dev):
+    """K7: the measured DFMA rate and the SM clock K7 ran at."""
+    import ctypes
+    from paper_1701_03512_b200 import _native
+    rate, mhz = ctypes.c_double(), ctypes.c_double()
+    _native.check(_native.lib().bp_fp64_peak(dev, ctypes.byref(rate), ctypes.byref(mhz)))
+    return rate.value, mhz.value
+
+
+def roofline(w, workload, k_ms, paths, sm_count, clk, dev):
+    """FP64-pipe roofline of the dominant kernel (K1, with K2 inside k_ms).
+
+    achieved = executed FP64-pipe ops per launch / kernel time, where the
+    executed ops per leaf test come from the committed ncu capture of this
+    instantiation (tools/ncu_opmix.py: DSETP + the per-group/per-node DFMA,
+    DADD, DMUL); a path has one leaf test per payoff.  peak = n_SM x 64 FP64
+    lanes x the SM clock seen during the timed region (nvidia-smi median;
+    K7's own clock when no sample exists) -- the FP64 pipe at the clock the
+    kernel ran at.  K7 (a DFMA microbenchmark) is reported beside it.
+    frac_w is the SURVEY §8d W-based figure (3 ops per path per payoff),
+    which can exceed 1 because K1 spends ~1.2 FP64 ops per leaf test."""
+    k7_rate, k7_mhz = fp64_peak(dev)
+    mhz = (clk or {}).get("sm_mhz") or k7_mhz
+    peak = sm_count * FP64_LANES_PER_SM * mhz * 1e6
+    tests = paths * len(w["kinds"])
+    c = load_counters(workload)
+    roof = {"bound": "fp64", "unit": "Tops/s (FP64 pipe)", "peak": peak / 1e12,
+            "peak_kind": f"{sm_count} SMs x {FP64_LANES_PER_SM} FP64 lanes x {mhz:.0f} MHz (SM clock sampled "
+                         "during the timed region)",
+            "kernel_ms": k_ms, "paths_per_launch": paths, "leaf_tests_per_launch": tests}
+    if c:
+        ops = tests * c["fp64_pipe_ops_per_leaf_test"]
+        roof.update({"achieved": ops / (k_ms * 1e-3) / 1e12, "frac": ops / (k_ms * 1e-3) / peak,
+                     "traffic": c["dram_bytes_read"] + c["dram_bytes_write"],
+                     "traffic_unit": "DRAM bytes per launch (ncu)",
+                     "fp64_ops_per_leaf_test": c["fp64_pipe_ops_per_leaf_test"],
+                     "ncu": {k: c[k] for k in ("fp64_pipe_active_pct", "issue_active_pct",
+                                               "warp_inst_per_32_leaf_tests", "fma_pipe_active_pct", "source")
+                             if k in c}})
+    else:
+        roof.update({"achieved": None, "frac": None, "traffic": None})
+    W = sum(W_OPS[k] for k in w["kinds"])
+    roof["frac_w"] = paths * W / (k_ms * 1e-3) / peak
+    roof["W_ops_per_path"] = W
+    roof["k7"] = {"dfma_per_s": k7_rate, "sm_mhz": k7_mhz,
+                  "frac_of_pipe_at_its_clock": k7_rate / (sm_count * FP64_LANES_PER_SM * k7_mhz * 1e6)
+                  if k7_mhz else None}
+    roof["fp32_context"] = {"peak_tflops": 2 * FP32_LANES_PER_SM * sm_count * mhz * 1e6 / 1e12,
+                            "note": "FMA-pipe peak at the same clock (FMA = 2 flops); the per-leaf test is an "
+                                    "FP64 compare, so K1 uses the FP32/FMA pipe only for integer address work "
+                                    "(ncu fma_pipe_active_pct)"}
+    return roof
 
 
 def secondary_configs(dev):
@@ -330,10 +481,7 @@ def run_ours(args):
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus:
-        args.gpus = world
-    dev = local
+    dev = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(dev)
     group = None
     if world > 1:
@@ -341,33 +489,26 @@ def run_ours(args):
     import __graft_entry__
     __graft_entry__.build()
     import paper_1701_03512_b200 as bp
-    from paper_1701_03512_b200 import _native
 
     wl, classic_crr = workloads()
     w = wl[args.workload]
     warmup = max(3, args.warmup)
 
     with ClockSampler(dev) as clk:
-        times, vals, sh, req, kinds = time_workload(w, classic_crr, args.steps, warmup, rank, world, dev, group)
+        times, vals, sh, req, kinds, detail = time_workload(w, classic_crr, args.steps, warmup, rank, world, dev,
+                                                            group)
     ms_local = sum(times) / len(times)
-    ms = ms_local
-    if world > 1:
-        t = torch.tensor([ms_local], dtype=torch.float64, device=f"cuda:{dev}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = _max_over_ranks(ms_local, world, dev)
     total_paths = 1 << w["N"]
     value = total_paths / (ms * 1e-3)
+    clocks = clk.summary()
 
     # config 3 (N = 36) in the same run
     extra = {}
     if args.workload == "config2" and not args.no_config3:
-        t3, v3, _, _, _ = time_workload(wl["config3"], classic_crr, max(2, args.steps // 4), 3, rank, world, dev,
-                                        group)
-        ms3 = sum(t3) / len(t3)
-        if world > 1:
-            t = torch.tensor([ms3], dtype=torch.float64, device=f"cuda:{dev}")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms3 = float(t.item())
+        t3, v3, _, _, _, _ = time_workload(wl["config3"], classic_crr, max(2, args.steps // 4), 3, rank, world,
+                                           dev, group)
+        ms3 = _max_over_ranks(sum(t3) / len(t3), world, dev)
         extra = {"value": (1 << 36) / (ms3 * 1e-3), "unit": "paths/s", "ms_per_step": ms3,
                  "asian_call": v3["asian-call"]}
 
@@ -383,46 +524,28 @@ def run_ours(args):
     # for N > 1 every rank takes part (value_exact_distributed: its shard + NCCL)
     e2e_s, e2e_path = e2e_seconds(bp, req, kinds, args, warmup, rank, world, dev, group)
 
+    per_rank_ms = _gather_ranks(ms_local, world, dev)
+    per_rank_kernel_ms = _gather_ranks(detail["kernel_ms"], world, dev)
+    per_rank_exchange_ms = _gather_ranks(detail.get("exchange_ms", 0.0), world, dev)
+
     if rank != 0:
         if world > 1:
             dist.barrier()
             dist.destroy_process_group()
         return 0
 
-    # roofline: FP64-pipe ops (W per path per payoff) / kernel time vs measured DFMA peak
-    peak = __import__("ctypes").c_double()
-    clk_mhz = __import__("ctypes").c_double()
-    _native.check(_native.lib().bp_fp64_peak(dev, __import__("ctypes").byref(peak),
-                                             __import__("ctypes").byref(clk_mhz)))
-    # the timed steps themselves (CUDA events on the launch stream): at N = 1 a
-    # step is K1 + K2 (K1 ~97 % of it, profiles/r1_launches_config2.csv), so
-    # this is a slightly conservative K1 duration; the best isolated K1 + K2
-    # launch is reported beside it
-    k_min_ms = kernel_share(w, classic_crr, dev)
-    k_ms = ms_local if world == 1 else k_min_ms  # N > 1: the timed step also holds the NCCL exchange
-    W = sum(W_OPS[k] for k in w["kinds"])
-    achieved = total_paths * W / (k_ms * 1e-3)
-    traffic, ncu = None, None
-    try:  # DRAM bytes per launch and pipe counters from the committed ncu --set full capture
-        tr = json.load(open(os.path.join(ROOT, "profiles", "r1_traffic.json")))[args.workload]
-        traffic = tr["dram_bytes_read"] + tr["dram_bytes_write"]
-        ncu = {k: tr[k] for k in ("fp64_pipe_active_pct", "issue_active_pct", "warp_inst_per_32_leaf_tests")}
-        ncu["note"] = ("W counts 3 FP64 ops per leaf and payoff; K1 spends ~1.3 (one DSETP + amortised group "
-                       "adds), so frac > 1 while the FP64 pipe is ~70 % busy and issue ~90 %")
-    except Exception:
-        pass
-    roof = {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak.value / 1e12, "unit": "Tops/s (FP64 pipe)",
-            "frac": achieved / peak.value, "traffic": traffic, "traffic_unit": "bytes/launch (ncu, DRAM)",
-            "kernel_ms": k_ms, "kernel_ms_source": "mean of the timed steps (K1 + K2, CUDA events)" if world == 1 else
-            "full valuation on one GPU, best of 5 (K1 + K2, CUDA events)",
-            "isolated_launch_min_ms": k_min_ms, "W_ops_per_path": W,
-            "peak_kind": "measured DFMA microbenchmark (bp_fp64_peak, K7) on this GPU", "ncu": ncu,
-            "nominal_peak_Tops": 148 * 64 * 1.965e9 / 1e12}
+    # roofline of the dominant kernel on this rank: its share of the super-blocks
+    first, count, n_sb = detail["superblocks"]
+    rank_paths = total_paths * count // n_sb
+    k_ms = ms_local if world == 1 else detail["kernel_ms"]
+    sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
+    roof = roofline(w, args.workload, k_ms, rank_paths, sm_count, clocks, dev)
+    roof["kernel_ms_source"] = ("mean of the timed steps (K1 + K2, CUDA events on the launch stream)" if world == 1
+                                else "rank 0's super-blocks alone (K1 + K2, CUDA events), no exchange")
 
     h2d = 8 * w["N"] + 7 * 8 + 4  # the tree + per-step probabilities handed to the C ABI
     e2e = {"value": total_paths / e2e_s, "unit": "paths/s", "h2d_bytes_per_step": h2d,
-           "d2h_bytes_per_step": 8 * 6 * 2 * sh.n_sb, "seconds_per_step": e2e_s,
-           "path": e2e_path}
+           "d2h_bytes_per_step": 8 * 6 * 2 * sh.n_sb, "seconds_per_step": e2e_s, "path": e2e_path}
 
     try:
         cpu = cpu_baseline(w, classic_crr) if world == 1 else None
@@ -434,13 +557,21 @@ def run_ours(args):
         "value": value, "unit": "paths/s", "n_gpus": world, "steps": args.steps, "warmup": warmup,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (BASELINE configs; tree parameters, no dataset)",
-        "config": {**workload_config(args.workload, w), "parallelism": f"superblock-shard x{world}",
-                   "l2": "flushed (256 MiB write) between timed steps", "engine": "affine-threshold" if sh.engine else
-                   "path-walk", "inner_bits": sh.inner_bits, "superblocks": sh.n_sb},
+        "config": workload_config(args.workload, w),
+        "impl_detail": {"parallelism": f"superblock-shard x{world} (one rank per GPU, NCCL all_gather)",
+                        "l2": "flushed (256 MiB write) between timed steps",
+                        "engine": "affine-threshold" if sh.engine else "path-walk", "inner_bits": sh.inner_bits,
+                        "superblocks": sh.n_sb, "leaf_block": "Gray-code predicate counting, per-class fold, "
+                                                             "2 nodes per table load"},
         "values": vals, "config3": extra or None, **extra45, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": launches_per_step * args.steps,
-        "clocks": clk.summary(),
+        "clocks": clocks,
     }
+    if world > 1:
+        line["scaling_detail"] = {"per_rank_step_ms": per_rank_ms, "per_rank_kernel_ms": per_rank_kernel_ms,
+                                  "per_rank_exchange_ms": per_rank_exchange_ms,
+                                  "note": "step = the rank's K1 + K2 and the NCCL all_gather; kernel / exchange "
+                                          "timed alone with CUDA events (means), max over ranks for the step"}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -448,17 +579,27 @@ def run_ours(args):
     return 0
 
 
-def main():
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="config2", choices=["config1", "config2", "config3"])
-    ap.add_argument("--no-config3", action="store_true")
-    args = ap.parse_args()
+    ap.add_argument("--no-config3", action="store_true", help="headline workload only (no secondary configs)")
+    ap.add_argument("--no-stock", action="store_true", help="reference arm: skip the stock-package baseline")
+    args = ap.parse_args(argv)
     if args.impl == "reference":
         return run_reference(args)
+    from paper_1701_03512_b200.launch import LaunchError, ensure_world
+    try:
+        rc = ensure_world(args.gpus, __file__, argv)
+    except LaunchError as exc:
+        print(f"bench.py: {exc}", file=sys.stderr)
+        return 2
+    if rc is not None:  # ran the ranks under torchrun
+        return rc
     return run_ours(args)
 
 

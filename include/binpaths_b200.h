@@ -196,7 +196,9 @@ void bp_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2],
                       uint32_t out[4]);
 
 /* Measured FP64-pipe peak (DFMA per second) of a device: a microbenchmark
- * of independent DFMA chains over every SM (K7 of SURVEY.md §2.3).        */
+ * of independent DFMA chains over every SM (K7 of SURVEY.md §2.3), and the
+ * SM clock it ran at (median over CTAs of clock64 cycles per globaltimer ns),
+ * so the rate can be compared with n_SM x 64 x clock.                      */
 int bp_fp64_peak(int device, double* dfma_per_s, double* sm_clock_mhz);
 
 int bp_device_count(void);

@@ -1223,27 +1223,35 @@ extern "C" int bp_fp64_peak(int device, double* dfma_per_s, double* sm_clock_mhz
   const int sms = device_sm_count(device);
   const int grid = sms * 8;
   double* buf = nullptr;
+  unsigned long long* clk = nullptr;
   BP_CUDA(cudaMalloc((void**)&buf, sizeof(double) * grid * 256));
+  BP_CUDA(cudaMalloc((void**)&clk, sizeof(unsigned long long) * 2 * grid));
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   BP_CUDA(launch_dfma_peak(buf, grid, 20, 0));
   const int iters = 2000;
   cudaEventRecord(e0, 0);
-  BP_CUDA(launch_dfma_peak(buf, grid, iters, 0));
+  BP_CUDA(launch_dfma_peak(buf, grid, iters, 0, clk));
   cudaEventRecord(e1, 0);
   BP_CUDA(cudaEventSynchronize(e1));
   float ms = 0.f;
   cudaEventElapsedTime(&ms, e0, e1);
+  std::vector<unsigned long long> h(2 * (size_t)grid);
+  BP_CUDA(cudaMemcpy(h.data(), clk, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost));
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   cudaFree(buf);
+  cudaFree(clk);
   const double ops = (double)grid * 256 * iters * 16 * 8;
   if (dfma_per_s) *dfma_per_s = ops / (ms * 1e-3);
   if (sm_clock_mhz) {
-    int khz = 0;
-    cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, device);
-    *sm_clock_mhz = khz / 1e3;
+    // the clock K7 ran at: median over CTAs of SM cycles / globaltimer ns
+    std::vector<double> mhz;
+    for (int b = 0; b < grid; ++b)
+      if (h[2 * b + 1] > 0) mhz.push_back(1e3 * (double)h[2 * b] / (double)h[2 * b + 1]);
+    std::sort(mhz.begin(), mhz.end());
+    *sm_clock_mhz = mhz.empty() ? 0.0 : mhz[mhz.size() / 2];
   }
   return BP_OK;
 }

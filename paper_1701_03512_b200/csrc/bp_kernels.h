@@ -59,7 +59,8 @@ cudaError_t launch_mc_shared(const McArgs& a, unsigned long long R, const double
                              double* stratum_means_dev, cudaStream_t st);
 unsigned long long mc_chunk();
 
-cudaError_t launch_dfma_peak(double* out, int grid, int iters, cudaStream_t st);
+cudaError_t launch_dfma_peak(double* out, int grid, int iters, cudaStream_t st,
+                             unsigned long long* clk = nullptr);
 
 // K1w per-leaf-weight enumeration (any per-step probabilities), bp_exact_w_kernels.cu
 cudaError_t launch_exact_w(unsigned km, const void* args, int grid, cudaStream_t st, double2* unit_out);
