@@ -5,9 +5,11 @@
 // CTA builds that option's tables in shared memory (each option has its own
 // u, d, p) -- the inner table sorted inside each up-count class by a rank
 // computation, the group prefix sums, the middle tables and the weights --
-// and then runs the same explicit leaf block as K1 (bp_leaf.cuh) over its
-// share of the option's thread prefixes, nodes in pairs.  Partials are
-// reduced in a fixed order (CTA tree, then ascending CTA index per option).
+// and then runs the same explicit leaf block as K1 (bp_leaf.cuh: Gray-code
+// predicate counting, each class folded into two per-node sums as it
+// completes) over its share of the option's thread prefixes, nodes in pairs.
+// Partials are reduced in a fixed order (CTA tree, then ascending CTA index
+// per option).
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -28,7 +30,10 @@ struct BatchArgs {
 };
 
 template <unsigned KIND>
-__global__ void __launch_bounds__(kBThreads, 3)
+#ifndef BP_K3_MINB
+#define BP_K3_MINB 3  // resident CTAs per SM targeted by K3
+#endif
+__global__ void __launch_bounds__(kBThreads, BP_K3_MINB)
 k_exact_batch(const BatchOption* __restrict__ opts, BatchArgs ba, double2* __restrict__ partial) {
   constexpr int NL = 1 << kBL, NC = kBL + 1, NMID = 1 << kBM, NG = n_groups(kBL), NP = kBNP;
   constexpr bool AC = KIND == kAC, AP = KIND == kAP, FL = KIND == kFL, FLP = KIND == kFLP, EC = KIND == kEC,
@@ -37,6 +42,8 @@ k_exact_batch(const BatchOption* __restrict__ opts, BatchArgs ba, double2* __res
   constexpr bool DESC = AC || FL;  // compare direction '>' -> sort descending
   __shared__ __align__(16) double tab[NL];
   __shared__ double gpre[NG * kGroupSlots];
+  __shared__ __align__(16) double2 sgray[TAB ? NG * kGraySlots : 1];
+  __shared__ double sW1[(FL || FLP) ? kMaxN + 2 : 1], sW2[(FL || FLP) ? kMaxN + 2 : 1];
   __shared__ double mid_c[NMID], mid_e[NMID], mid_x[NMID];
   __shared__ int mid_h[NMID];
   __shared__ double w[kMaxN + 2 + NC];
@@ -121,6 +128,23 @@ k_exact_batch(const BatchOption* __restrict__ opts, BatchArgs ba, double2* __res
       for (int k = 0; k < n && k < len; ++k) comp_add(s, cc, tab[i0 + k]);
       gpre[gi] = s + cc;
     }
+  // lookback kinds: per node up count h, W1[h] = sum_c w[h+c] C(L,c) and
+  // W2[h] = sum_c w[h+c] C(L,c) e_c (out-of-the-money and terminal terms)
+  if (FL || FLP)
+    for (int h = tid; h < kMaxN + 2; h += kBThreads) {
+      double w1 = 0.0, w2 = 0.0;
+      for (int c = 0; c < NC; ++c) {
+        w1 = fma(w[h + c], b_cls[c], w1);
+        w2 = fma(w[h + c] * b_cls[c], e_cls[c], w2);
+      }
+      sW1[h] = w1;
+      sW2[h] = w2;
+    }
+  __syncthreads();
+  // Gray-ordered {prefix sum, count} tables (count as a double: the fold form)
+  if (TAB)
+    for (int i = tid; i < NG * kGraySlots; i += kBThreads)
+      sgray[i] = gray_table_entry(&gpre[(i / kGraySlots) * kGroupSlots], (unsigned)(i % kGraySlots), true);
   __syncthreads();
 
   const double NK = (double)N * o.K;
@@ -155,26 +179,34 @@ k_exact_batch(const BatchOption* __restrict__ opts, BatchArgs ba, double2* __res
         const double rS = 1.0 / Sn[p];
         th[p] = (AC || AP) ? -base[p] * rS : FL ? Xn[p] * rS : FLP ? fmin(Xn[p], o.K) * rS : 0.0;
       }
-      double acc[NP][NC];
-      int cnt[NP][NC];
-      zero_acc<NP, NC>(acc, cnt);
-      if (TAB) leaf_block<kBL, NP, 0, DESC>(reinterpret_cast<const double2*>(tab) + (j0 & zero), gpre, th, acc, cnt);
+      if (TAB) {
+        // node value, affine in sA = sum_c w[h+c] A_c and sN = sum_c w[h+c] n_c
+        // (the K1 fold forms, bp_exact_fast.cuh)
+        double sA[NP], sN[NP];
+        leaf_block_fold<kBL, NP, 0, DESC>(reinterpret_cast<const double2*>(tab) + (j0 & zero),
+                                          reinterpret_cast<const char*>(sgray), w, hn, th, sA, sN);
 #pragma unroll
-      for (int p = 0; p < NP; ++p) {
-        double val = 0.0;
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-          const double n = (double)cnt[p][c], bc = b_cls[c];
-          double contrib = 0.0;
-          if (AC) contrib = fma(Sn[p], acc[p][c], base[p] * n);
-          if (AP) contrib = fma(-Sn[p], acc[p][c], -base[p] * n);
-          if (FL) contrib = fma(-Sn[p] * e_cls[c], bc, fma(Sn[p], acc[p][c], Xn[p] * (bc - n)));
-          if (FLP) contrib = fma(bc - n, fmax(o.K - Xn[p], 0.0), fma(o.K, n, -Sn[p] * acc[p][c]));
-          if (EC) contrib = bc * fmax(fma(Sn[p], e_cls[c], -o.K), 0.0);
-          if (EP) contrib = bc * fmax(fma(-Sn[p], e_cls[c], o.K), 0.0);
-          val = fma(w[hn[p] + c], contrib, val);
+        for (int p = 0; p < NP; ++p) {
+          double val;
+          if (AC) val = fma(Sn[p], sA[p], base[p] * sN[p]);
+          if (AP) val = -fma(Sn[p], sA[p], base[p] * sN[p]);
+          if (FL) val = fma(Sn[p], sA[p] - sW2[hn[p]], Xn[p] * (sW1[hn[p]] - sN[p]));
+          if (FLP) val = fma(fmax(o.K - Xn[p], 0.0), sW1[hn[p]] - sN[p], fma(o.K, sN[p], -Sn[p] * sA[p]));
+          comp_add(ts, tc, val);
         }
-        comp_add(ts, tc, val);
+      } else {
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          double val = 0.0;
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            const double bc = b_cls[c];
+            const double contrib = EC ? bc * fmax(fma(Sn[p], e_cls[c], -o.K), 0.0)
+                                      : bc * fmax(fma(-Sn[p], e_cls[c], o.K), 0.0);
+            val = fma(w[hn[p] + c], contrib, val);
+          }
+          comp_add(ts, tc, val);
+        }
       }
     }
   }

@@ -259,6 +259,54 @@ static void kind_table_layout(int kind, const std::vector<double>& c, const std:
   }
 }
 
+// I15 screen tables of one slot (bp_exact.cuh, bp_leaf.cuh I15Class): per big
+// class a monotone map onto [0, 32767] spanning the class's values
+// (increasing for '>' kinds, decreasing for '<' kinds, so that in both cases
+// a screened value above the threshold's proves the leaf in the money), the
+// screened value of every position in both 16-bit lanes, and the class
+// prefix sums in sorted order (compensated, rounded once).
+template <int L>
+static void i15_layout(int kind, const double* pos, ExactArgs<L>& a, int slot) {
+  const bool desc = (kind == kAC || kind == kFL);
+  for (int c = 0; c <= L; ++c) {
+    a.nrm_s[slot][c] = 1.0f;
+    a.nrm_o[slot][c] = kI15Magic;
+    if (!i15_class(L, c)) continue;
+    const int i0 = class_start(L, c), len = binom(L, c);
+    float lo = (float)pos[i0], hi = (float)pos[i0];
+    for (int j = 0; j < len; ++j) {
+      lo = std::min(lo, (float)pos[i0 + j]);
+      hi = std::max(hi, (float)pos[i0 + j]);
+    }
+    // the class spans the codes [4, 32763]: a clamped threshold (0 or
+    // 32767) never equals a screened value; |v s| <= 2^22 keeps the fp32
+    // products resolved to half a code
+    const float range = hi - lo, amax = std::max(std::fabs(lo), std::fabs(hi));
+    double sc = range > 0.0f ? 32759.0 / (double)range : 1.0;
+    if (amax > 0.0f) sc = std::min(sc, 4194304.0 / (double)amax);
+    if (!(sc > 0.0) || !std::isfinite(sc)) sc = 1.0;
+    const float sf = (float)(desc ? sc : -sc);
+    // the end of the range the map sends to code 4
+    const double o = (double)kI15Magic + 4.0 - (double)(desc ? lo : hi) * (double)sf;
+    a.nrm_s[slot][c] = sf;
+    a.nrm_o[slot][c] = std::isfinite(o) ? (float)o : kI15Magic;
+    for (int j = 0; j < len; ++j) {
+      int e = j + 1;
+      const double tol = std::ldexp(std::fabs(pos[i0 + j]), -44);
+      while (e < len && std::fabs(pos[i0 + e] - pos[i0 + j]) <= tol) ++e;
+      a.te[slot][i0 + j] = (unsigned char)e;
+    }
+    double sum = 0.0, comp = 0.0;
+    a.cpre[slot][i0 + c] = 0.0;
+    for (int j = 0; j < len; ++j) {
+      const unsigned k = i15_map((float)pos[i0 + j], a.nrm_s[slot][c], a.nrm_o[slot][c]);
+      a.xq[slot][i0 + j] = k | (k << 16);
+      comp_add(sum, comp, pos[i0 + j]);
+      a.cpre[slot][i0 + c + j + 1] = sum + comp;
+    }
+  }
+}
+
 template <int L>
 static int fill_fast_args(const bp_tree* t, const Layout& lay, unsigned km, std::vector<unsigned char>& buf) {
   buf.assign(sizeof(ExactArgs<L>), 0);
@@ -276,6 +324,7 @@ static int fill_fast_args(const bp_tree* t, const Layout& lay, unsigned km, std:
   for (int slot = 0; slot < nt; ++slot) {
     kind_table_layout<L>(kinds[slot], c, mx, mn, pos.data(), a.gpre[slot]);
     for (int i = 0; i < (1 << L); ++i) a.tab[slot * (1 << L) + i] = pos[i];
+    if constexpr (i15_on<L>()) i15_layout<L>(kinds[slot], pos.data(), a, slot);
   }
   // middle tables (chunk of m steps)
   const int m = lay.m;
@@ -482,7 +531,11 @@ static std::vector<unsigned> fast_groups(uint32_t payoffs) {
   std::vector<unsigned> g;
   unsigned rest = payoffs;
   const unsigned pair = (1u << kAC) | (1u << kFL);
-  if ((rest & pair) == pair) {
+  static const bool fuse = [] {  // diagnostics: BINPATHS_FUSE_ACFL=0 launches the pair apart
+    const char* e = std::getenv("BINPATHS_FUSE_ACFL");
+    return !e || std::atoi(e) != 0;
+  }();
+  if (fuse && (rest & pair) == pair) {
     g.push_back(pair);
     rest &= ~pair;
   }
@@ -567,14 +620,23 @@ struct bp_exact_plan {
   Scratch scratch[64];
   std::mutex mu;
   // captured enqueues of the class engine, keyed by (device, super-block
-  // range, output buffer, scratch): a repeated enqueue is one graph launch
+  // range, output buffer, scratch): a repeated enqueue is one graph launch.
+  // A key is captured the second time it is seen in a row (a caller with a
+  // fresh output buffer per call keeps the ordinary launches), and at most
+  // kMaxPlanGraphs stay instantiated (least recently used out first).
   struct Graph {
     int dev, sb_first, sb_count;
     double* out;
     double2* scratch;
     cudaGraphExec_t exec;
+    bool same(const Graph& o) const {
+      return dev == o.dev && sb_first == o.sb_first && sb_count == o.sb_count && out == o.out &&
+             scratch == o.scratch;
+    }
   };
-  std::vector<Graph> graphs;
+  static constexpr size_t kMaxPlanGraphs = 8;
+  std::list<Graph> graphs;
+  Graph last_miss{-1, 0, 0, nullptr, nullptr, nullptr};
 };
 
 static int plan_build(const bp_tree* t, uint32_t payoffs, uint32_t flags, bp_exact_plan* P) {
@@ -861,10 +923,16 @@ static bool plan_enqueue_graph(bp_exact_plan* P, int dev, int sb_first, int sb_c
     scratch = P->scratch[dev].p;
     const size_t need = sizeof(double2) * kNumKinds * (unsigned long long)sb_count * P->lay.units_per_sb;
     if (!scratch || P->scratch[dev].bytes < need) return false;  // not sized yet: ordinary path first
-    for (auto& gr : P->graphs)
-      if (gr.dev == dev && gr.sb_first == sb_first && gr.sb_count == sb_count && gr.out == out_dev &&
-          gr.scratch == scratch)
-        return cudaGraphLaunch(gr.exec, st) == cudaSuccess;
+    const bp_exact_plan::Graph key{dev, sb_first, sb_count, out_dev, scratch, nullptr};
+    for (auto it = P->graphs.begin(); it != P->graphs.end(); ++it)
+      if (it->same(key)) {
+        P->graphs.splice(P->graphs.begin(), P->graphs, it);  // most recently used first
+        return cudaGraphLaunch(it->exec, st) == cudaSuccess;
+      }
+    if (!P->last_miss.same(key)) {  // first sighting: ordinary launches, capture on a repeat
+      P->last_miss = key;
+      return false;
+    }
   }
   for (auto& g : P->groups) cached_occupancy_fast(P->lay.L, g.km, false);  // no queries inside the capture
   cudaStream_t cap;
@@ -885,7 +953,11 @@ static bool plan_enqueue_graph(bp_exact_plan* P, int dev, int sb_first, int sb_c
   }
   {
     std::lock_guard<std::mutex> g(P->mu);
-    P->graphs.push_back(bp_exact_plan::Graph{dev, sb_first, sb_count, out_dev, scratch, exec});
+    P->graphs.push_front(bp_exact_plan::Graph{dev, sb_first, sb_count, out_dev, scratch, exec});
+    if (P->graphs.size() > bp_exact_plan::kMaxPlanGraphs) {
+      cudaGraphExecDestroy(P->graphs.back().exec);
+      P->graphs.pop_back();
+    }
   }
   return cudaGraphLaunch(exec, st) == cudaSuccess;
 }

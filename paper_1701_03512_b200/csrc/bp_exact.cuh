@@ -33,7 +33,9 @@
 //   the node value is sum_c w[h + c] (S A_c + base n_c), w[h] =
 //   e^{-qT} p^h (1-p)^{N-h} (exact.py:95,99 folded into one table).
 #pragma once
+#include <cmath>
 #include <cstdint>
+#include <cstring>
 #include "bp_common.cuh"
 
 namespace bp {
@@ -113,12 +115,76 @@ constexpr int kNodesPerBlock = BP_NP;
 constexpr int kNodesPerBlockLog2 = BP_NP == 4 ? 2 : BP_NP == 2 ? 1 : 0;
 static_assert(BP_NP == 1 || BP_NP == 2 || BP_NP == 4, "BP_NP must be 1, 2 or 4");
 
+// BP_I15 -- the big classes (>= kI15Min leaves) of the K1 leaf block (L = 8,
+//           two nodes per block, fold mode) screen their leaves with a 15-bit
+//           fixed-point compare: two nodes per 32-bit integer multiply-add,
+//           the sign bits XOR-ed into Gray-code counters, and the rare
+//           ambiguous boundary leaf resolved in fp64 (bp_leaf.cuh, I15Class).
+#ifndef BP_I15
+#define BP_I15 1
+#endif
+constexpr int kI15Min = 16;
+template <int L>
+__host__ __device__ constexpr bool i15_on() {
+  return BP_I15 && BP_FOLD && BP_GRAY && L == 8 && kNodesPerBlock == 2;
+}
+__host__ __device__ constexpr bool i15_class(int L, int c) { return binom(L, c) >= kI15Min; }
+__host__ __device__ constexpr int bit_length(int v) {
+  int b = 0;
+  while (v >> b) ++b;
+  return b;
+}
+// Gray-code counter slots of a class (codes of the counts 0..|c|) and their
+// offset in the per-slot entry table
+__host__ __device__ constexpr int i15_slots(int L, int c) { return 1 << bit_length(binom(L, c)); }
+__host__ __device__ constexpr int i15_base(int L, int c) {
+  int s = 0;
+  for (int i = 0; i < c; ++i)
+    if (i15_class(L, i)) s += i15_slots(L, i);
+  return s;
+}
+__host__ __device__ constexpr int i15_entries(int L) { return i15_base(L, L + 1); }
+
+// The monotone map of the screen: v -> k in [0, 32767], k = clamp(round(vf *
+// s + o)) evaluated in fp32 with one fused multiply-add (o carries 1.5 * 2^23,
+// so the fp32 result is an integer).  Host (table values) and device (node
+// thresholds) evaluate the same IEEE operations, so v1 <= v2 implies
+// k(v1) <= k(v2) for s > 0 (>= for s < 0): k(x) > k(theta) proves x > theta,
+// k(x) < k(theta) proves x < theta, and only k(x) == k(theta) is ambiguous.
+// A NaN threshold maps to 32767 (no leaf is screened in).
+constexpr float kI15Magic = 12582912.0f;
+__host__ __device__ inline unsigned i15_map(float vf, float s, float o) {
+#ifdef __CUDA_ARCH__
+  float f = __fmaf_rn(vf, s, o);
+  f = fmaxf(fminf(f, kI15Magic + 32767.0f), kI15Magic);
+  return __float_as_uint(f) - 0x4B400000u;
+#else
+  float f = std::fma(vf, s, o);
+  f = std::fmax(std::fmin(f, kI15Magic + 32767.0f), kI15Magic);
+  unsigned u;
+  std::memcpy(&u, &f, sizeof u);
+  return u - 0x4B400000u;
+#endif
+}
+
 template <int L>
 struct __align__(16) ExactArgs {
   // inner tables by position (class-major, sorted in the compare direction
   // inside a class), slot-major: tab[slot * 2^L + i]
   double tab[2 << L];
   double gpre[2][n_groups(L)][kGroupSlots];  // group prefix sums per slot
+  // I15 screen (i15_on<L>()), per slot: the screened value k of every
+  // position in both 16-bit lanes (k | k << 16), the per-class map (scale,
+  // offset) and the class prefix sums P_c[n], n = 0..|c|, at
+  // cpre[slot][class_start(L, c) + c + n]
+  __align__(16) unsigned xq[2][i15_on<L>() ? (1 << L) : 4];
+  // end (exclusive, class-relative) of the tie run starting at each
+  // position: the following positions whose value is within 2^-44 relative
+  // of it (a leaf whose value ties with the threshold's to that precision
+  // contributes ~0 either way, so a tie run is classified as one leaf)
+  unsigned char te[2][i15_on<L>() ? (1 << L) : 4];
+  double cpre[2][i15_on<L>() ? (1 << L) + L + 1 : 1];
+  float nrm_s[2][L + 1], nrm_o[2][L + 1];
   double mid_c[kMidMax], mid_e[kMidMax], mid_mx[kMidMax], mid_mn[kMidMax];
   int mid_h[kMidMax];
   double w[kMaxN + 2];    // e^{-qT} p^h (1-p)^{N-h}, h = 0..N (zero padded)

@@ -17,6 +17,18 @@
 
 namespace bp {
 
+// 1 / x without the library's out-of-range call (x is a positive normal node
+// price): the MUFU estimate and two Newton steps (relative error ~1 ulp; the
+// thresholds it feeds decide only leaves whose payoff is within rounding of 0)
+__device__ __forceinline__ double fast_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
 
 // resident CTAs per SM the register allocation targets: 3 for one table
 // (<= 85 registers), 2 for the fused two-table kernels (measured best, r1)
@@ -49,11 +61,33 @@ k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_
   __shared__ double sw[kMaxN + 2 + NC];
   __shared__ unsigned long long shist[kMaxN + 2];
 #if BP_GRAY
-  __shared__ __align__(16) double2 sgray[NT > 0 ? NT : 1][NG * kGraySlots];
-  for (int t = 0; t < NT; ++t)
+  // I15 screen on the Asian slot (slot 0; the lookback thresholds are ratios
+  // of lattice prices that tie with the table values, so those kinds keep the
+  // fp64 block): its entry tables, screened values and tie-run ends, and the
+  // Gray tables of the classes it leaves to the fp64 block; the other slot
+  // keeps all its Gray tables
+  constexpr bool I15 = i15_on<L>() && (kAC_ || kAP_);
+  constexpr int NG0 = I15 ? n_small_groups<L>() : NG;
+  __shared__ __align__(16) double2 sgray0[NT > 0 ? NG0 * kGraySlots : 1];
+  __shared__ __align__(16) double2 sgray1[NT > 1 ? NG * kGraySlots : 1];
+  __shared__ __align__(16) double2 si15[I15 ? 2 * i15_entries(L) : 1];
+  __shared__ __align__(16) unsigned sxq[I15 ? (1 << L) : 4];
+  __shared__ unsigned char ste[I15 ? (1 << L) : 4];
+  if constexpr (I15) {
+    gray_fill_small<L, 0>(a.gpre[0], sgray0);
+    i15_fill<L, 0>(a, 0, si15);
+    for (int i = threadIdx.x; i < (1 << L); i += blockDim.x) {
+      sxq[i] = a.xq[0][i];
+      ste[i] = a.te[0][i];
+    }
+  } else if constexpr (NT > 0) {
     for (int i = threadIdx.x; i < NG * kGraySlots; i += blockDim.x)
-      sgray[t][i] = gray_table_entry(&a.gpre[t][i / kGraySlots][0], (unsigned)(i % kGraySlots), BP_FOLD != 0);
-#define BP_GTAB(SLOT) reinterpret_cast<const char*>(&sgray[SLOT][0])
+      sgray0[i] = gray_table_entry(&a.gpre[0][i / kGraySlots][0], (unsigned)(i % kGraySlots), BP_FOLD != 0);
+  }
+  if constexpr (NT > 1)
+    for (int i = threadIdx.x; i < NG * kGraySlots; i += blockDim.x)
+      sgray1[i] = gray_table_entry(&a.gpre[1][i / kGraySlots][0], (unsigned)(i % kGraySlots), BP_FOLD != 0);
+#define BP_GTAB(SLOT) reinterpret_cast<const char*>((SLOT) == 0 ? &sgray0[0] : &sgray1[0])
 #define BP_LEAF(SLOT, GTV, TH) leaf_block_gray<L, NP, SLOT, GTV>(tb, BP_GTAB(SLOT), TH, acc, cnt)
 #else
   __shared__ double sgpre[NT > 0 ? NT : 1][NG * kGroupSlots];
@@ -115,6 +149,9 @@ k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_
 
     // nodes are processed NP at a time (n_mid is a multiple of NP: m >= 1)
     for (int j0 = 0; j0 < sc.n_mid; j0 += NP) {
+      // table offset 0, opaque (the loads stay inside the loop) and, as a
+      // warp reduction, held in a uniform register (uniform LDCU loads)
+      const int zoff = (int)__reduce_or_sync(0xffffffffu, (unsigned)(j0 & sc.zero));
       double Sn[NP], Sg[NP], Mxn[NP], Mnn[NP], base[NP], thC[NP], thX[NP], thN[NP];
       int hn[NP];
 #pragma unroll
@@ -127,29 +164,41 @@ k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_
         Mnn[p] = needMn ? fmin(Mn, S * a.mid_mn[j]) : 0.0;
         hn[p] = h + a.mid_h[j];
         base[p] = Sg[p] - sc.NK;
-        const double rS = 1.0 / Sn[p];
+        const double rS = fast_rcp(Sn[p]);
         thC[p] = (kAC_ || kAP_) ? -base[p] * rS : 0.0;
         thX[p] = kFL_ ? Mxn[p] * rS : 0.0;
         thN[p] = kFLP_ ? fmin(Mnn[p], sc.K) * rS : 0.0;
       }
 
 #if BP_TAB_SMEM
-      const double2* tb = reinterpret_cast<const double2*>(stab) + (j0 & sc.zero);  // + 0, opaque
+      const double2* tb = reinterpret_cast<const double2*>(stab) + zoff;  // + 0, opaque
 #else
-      const double2* tb = reinterpret_cast<const double2*>(a.tab) + (j0 & sc.zero);  // + 0, opaque
+      const double2* tb = reinterpret_cast<const double2*>(a.tab) + zoff;  // + 0, opaque
 #endif
       // --- per kind: the leaf block (2^L explicit leaf tests per node), then
       // the class finalisation, node value = sum_c w[h+c] * contrib_c.  Kinds
       // run one after the other so only one kind's accumulators are live.
 #if BP_FOLD
+      // the leaf block of a slot: I15 screen on slot 0 of the Asian kinds
+#define BP_FOLDLEAF(SLOT, GTV, TH)                                                                            \
+  if constexpr (I15 && (SLOT) == 0)                                                                          \
+    leaf_block_fold_i15<L, SLOT, GTV>(a, reinterpret_cast<const uint4*>(sxq) + zoff,                        \
+                                      I15Ctx{reinterpret_cast<const char*>(si15), sxq, ste,                  \
+                                             1u | (unsigned)sc.zero, {0.f, 0.f}},                           \
+                                      tb, BP_GTAB(SLOT), sw, hn, TH, sA, sN);                                \
+  else                                                                                                       \
+    leaf_block_fold<L, NP, SLOT, GTV>(tb, BP_GTAB(SLOT), sw, hn, TH, sA, sN)
       // node value, affine in sA = sum_c w[h+c] A_c and sN = sum_c w[h+c] n_c
       // (A_c / n_c: class-c in-the-money table sum and count):
       //   AC  S sA + base sN              AP  -(S sA + base sN)
       //   FL  S (sA - W2) + Mx (W1 - sN)  FLP K sN - S sA + max(K - Mn, 0) (W1 - sN)
       if (kAC_ || kAP_) {
         double sA[NP], sN[NP];
-        if (kAC_) leaf_block_fold<L, NP, slotAC, true>(tb, BP_GTAB(slotAC), sw, hn, thC, sA, sN);
-        else leaf_block_fold<L, NP, slotAP, false>(tb, BP_GTAB(slotAP), sw, hn, thC, sA, sN);
+        if constexpr (kAC_) {
+          BP_FOLDLEAF(slotAC, true, thC);
+        } else {
+          BP_FOLDLEAF(slotAP, false, thC);
+        }
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
           const double v = fma(Sn[p], sA[p], base[p] * sN[p]);
@@ -159,14 +208,14 @@ k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_
       }
       if (kFL_) {
         double sA[NP], sN[NP];
-        leaf_block_fold<L, NP, slotFL, true>(tb, BP_GTAB(slotFL), sw, hn, thX, sA, sN);
+        BP_FOLDLEAF(slotFL, true, thX);
 #pragma unroll
         for (int p = 0; p < NP; ++p)
           comp_add(ts[kFL], tc[kFL], fma(Sn[p], sA[p] - sW2[hn[p]], Mxn[p] * (sW1[hn[p]] - sN[p])));
       }
       if (kFLP_) {
         double sA[NP], sN[NP];
-        leaf_block_fold<L, NP, slotFLP, false>(tb, BP_GTAB(slotFLP), sw, hn, thN, sA, sN);
+        BP_FOLDLEAF(slotFLP, false, thN);
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
           const double flat = fmax(sc.K - Mnn[p], 0.0);
@@ -286,6 +335,7 @@ k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_
 
 #undef BP_LEAF
 #undef BP_GTAB
+#undef BP_FOLDLEAF
 
 // launch wrappers
 template <int L, unsigned KM>

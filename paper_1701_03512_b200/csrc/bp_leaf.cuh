@@ -149,7 +149,20 @@ __device__ __forceinline__ void leaf_block_gray(const double2* __restrict__ tb, 
 // (A_c = sum of the class's in-the-money table values, n_c their count, both
 // read from the Gray tables with n as a double).  The kinds' node values are
 // affine in (sA, sN), see k_exact_fast.
-template <int L, int NP, int SLOT, bool GT, int C, int G>
+// Gray-table group index of (class C, group 0): all classes, or (CMP) only the
+// classes the I15 screen leaves to this block
+template <int L, bool CMP>
+__host__ __device__ constexpr int gray_group_base(int C) {
+  if (!CMP) return group_base(L, C);
+  int s = 0;
+  for (int i = 0; i < C; ++i)
+    if (!i15_class(L, i)) s += class_groups(L, i);
+  return s;
+}
+template <int L>
+__host__ __device__ constexpr int n_small_groups() { return gray_group_base<L, true>(L + 1); }
+
+template <int L, int NP, int SLOT, bool GT, int C, int G, bool CMP = false>
 struct FoldGroups {
   static __device__ __forceinline__ void run(const double2* __restrict__ tb, const char* __restrict__ gtab,
                                              const double (&th)[NP], double (&A)[NP], double (&n)[NP]) {
@@ -166,14 +179,14 @@ struct FoldGroups {
       }
       unsigned off[NP];
       gray_count<len, GT, NP>(x, th, off);
-      const char* grp = gtab + (group_base(L, C) + G) * kGraySlots * kGrayEntry;
+      const char* grp = gtab + (gray_group_base<L, CMP>(C) + G) * kGraySlots * kGrayEntry;
 #pragma unroll
       for (int p = 0; p < NP; ++p) {
         const double2 e = *reinterpret_cast<const double2*>(grp + off[p]);
         A[p] = G == 0 ? e.x : A[p] + e.x;
         n[p] = G == 0 ? e.y : n[p] + e.y;
       }
-      FoldGroups<L, NP, SLOT, GT, C, G + 1>::run(tb, gtab, th, A, n);
+      FoldGroups<L, NP, SLOT, GT, C, G + 1, CMP>::run(tb, gtab, th, A, n);
     }
   }
 };
@@ -202,6 +215,181 @@ __device__ __forceinline__ void leaf_block_fold(const double2* __restrict__ tb, 
                                                 const double* __restrict__ sw, const int (&hn)[NP],
                                                 const double (&th)[NP], double (&sA)[NP], double (&sN)[NP]) {
   FoldClasses<L, NP, SLOT, GT, 0>::run(tb, gtab, sw, hn, th, sA, sN);
+}
+
+// ---------------------------------------------------------------------------
+// I15 screen of one big class for a node pair (node 0 in the low 16-bit lane,
+// node 1 in the high lane).  Every leaf j is tested explicitly: one 32-bit
+// multiply-add x_j * 1 + T forms, per lane, x~_j + 0x7FFF - theta~, whose
+// bit 15 is set iff x~_j > theta~ (x~, theta~ = i15_map of the leaf value and
+// of the node threshold, both <= 0x7FFF, so no carry crosses the lanes).  The
+// result XORs into Gray-code counter bit ctz(j + 1) (the sorted class has its
+// surely-in-the-money leaves as a prefix, so after the class the counters
+// hold the Gray code of that prefix length n' per lane).  The code indexes
+// the class's 32-byte entry {P_c[n'], n', x~_n' | P_c[m], x_n'}, m = the
+// end of the tie run at n' (ExactArgs::te).  The only leaves whose
+// screen is not decisive have x~ == theta~ and start at position n': a lane
+// whose entry has x~_n' == theta~ tests leaf n' in fp64 (x_n' is in the
+// entry; an in-the-money leaf takes its tie run with it) and, in the rarer
+// case that position m has the same screened value too, walks on.
+struct I15Ctx {
+  const char* etab;          // the slot's entry table (shared memory)
+  const unsigned* sxq;       // the slot's screened values (shared memory)
+  const unsigned char* ste;  // the slot's tie-run ends (shared memory)
+  unsigned one;         // 1, opaque to the compiler (keeps the multiply-add an IMAD)
+  float thf[2];         // node thresholds in fp32
+};
+constexpr int kI15Entry = 32;  // bytes per entry
+
+__host__ __device__ constexpr int ctz_c(int v) {
+  int b = 0;
+  while (!((v >> b) & 1)) ++b;
+  return b;
+}
+
+template <int L, int SLOT, bool GT, int C>
+struct I15Class {
+  static constexpr int len = binom(L, C), nb = bit_length(len), i0 = class_start(L, C);
+  static __device__ __forceinline__ void run(const ExactArgs<L>& a, const uint4* __restrict__ xb, const I15Ctx& x,
+                                             const double (&th)[2], double (&A)[2], double (&n)[2]) {
+    const float s = a.nrm_s[SLOT][C], o = a.nrm_o[SLOT][C];
+    const unsigned k0 = i15_map(x.thf[0], s, o), k1 = i15_map(x.thf[1], s, o);
+    const unsigned T = __byte_perm(0x7FFFu - k0, 0x7FFFu - k1, 0x5410);
+    unsigned g[nb];
+#pragma unroll
+    for (int b = 0; b < nb; ++b) g[b] = 0u;
+#pragma unroll
+    for (int j = 0; j < len; ++j) {
+      const uint4 w = xb[(i0 + j) >> 2];
+      const int r = (i0 + j) & 3;
+      const unsigned xv = r == 0 ? w.x : r == 1 ? w.y : r == 2 ? w.z : w.w;
+      unsigned d;
+      asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(xv), "r"(x.one), "r"(T));
+      g[ctz_c(j + 1)] ^= d;
+    }
+    // byte offsets of the two lanes' codes: lane 1's bits (bit 31 of each
+    // counter) shift in from the top, lane 0's (bit 15) are masked and added
+    unsigned c1 = 0u, c0 = 0u;
+#pragma unroll
+    for (int b = nb - 1; b >= 0; --b) c1 = __funnelshift_l(g[b], c1, 1);
+#pragma unroll
+    for (int b = 0; b < nb; ++b) c0 += (g[b] & 0x8000u) << b;
+    const char* et0 = x.etab + i15_base(L, C) * kI15Entry + (c0 >> 10);
+    const char* et1 = x.etab + i15_base(L, C) * kI15Entry + (c1 << 5);
+    const double2 e0 = *reinterpret_cast<const double2*>(et0);
+    const double2 e1 = *reinterpret_cast<const double2*>(et1);
+    double2 r0 = make_double2(e0.x, (double)__int_as_float(__double2loint(e0.y)));
+    double2 r1 = make_double2(e1.x, (double)__int_as_float(__double2loint(e1.y)));
+    const bool amb0 = (unsigned)__double2hiint(e0.y) == k0, amb1 = (unsigned)__double2hiint(e1.y) == k1;
+    // warp-uniform branch (the surrounding control flow stays uniform)
+    if (__any_sync(0xffffffffu, amb0 || amb1)) {
+      fix(a, x, et0, th[0], k0, amb0, r0);
+      fix(a, x, et1, th[1], k1, amb1, r1);
+    }
+    A[0] = r0.x;
+    n[0] = r0.y;
+    A[1] = r1.x;
+    n[1] = r1.y;
+  }
+  // leaf n' in fp64 from the entry (with its tie run); a further leaf with
+  // the threshold's screened value takes the exact walk
+  static __device__ __forceinline__ void fix(const ExactArgs<L>& a, const I15Ctx& x, const char* et, double th,
+                                             unsigned k, bool amb, double2& r) {
+    if (!amb) return;
+    const double2 e1 = *reinterpret_cast<const double2*>(et + 16);  // {P_c[m], x_n'}
+    if (GT ? e1.y > th : e1.y < th) {
+      const int m = x.ste[i0 + (int)r.y];
+      r = make_double2(e1.x, (double)m);
+      if (m < len && (x.sxq[i0 + m] & 0xFFFFu) == k) r = walk(a, x, th, k, m);
+    }
+  }
+  static __device__ __noinline__ double2 walk(const ExactArgs<L>& a, const I15Ctx& x, double th, unsigned k, int j) {
+    while (j < len && (x.sxq[i0 + j] & 0xFFFFu) == k) {
+      const double v = a.tab[SLOT * (1 << L) + i0 + j];
+      if (!(GT ? v > th : v < th)) break;
+      j = x.ste[i0 + j];
+    }
+    return make_double2(a.cpre[SLOT][i0 + C + j], (double)j);
+  }
+};
+
+// K1 leaf block with the I15 screen on the big classes and the Gray fp64
+// block (FoldGroups) on the others; per class the fold as leaf_block_fold.
+template <int L, int SLOT, bool GT, int C>
+struct FoldClassesI15 {
+  static __device__ __forceinline__ void run(const ExactArgs<L>& a, const uint4* __restrict__ xb, const I15Ctx& x,
+                                             const double2* __restrict__ tb, const char* __restrict__ gtab,
+                                             const double* __restrict__ sw, const int (&hn)[2],
+                                             const double (&th)[2], double (&sA)[2], double (&sN)[2]) {
+    if constexpr (C <= L) {
+      double A[2], n[2];
+      if constexpr (i15_class(L, C))
+        I15Class<L, SLOT, GT, C>::run(a, xb, x, th, A, n);
+      else
+        FoldGroups<L, 2, SLOT, GT, C, 0, true>::run(tb, gtab, th, A, n);
+#pragma unroll
+      for (int p = 0; p < 2; ++p) {
+        const double w = sw[hn[p] + C];
+        sA[p] = C == 0 ? w * A[p] : fma(w, A[p], sA[p]);
+        sN[p] = C == 0 ? w * n[p] : fma(w, n[p], sN[p]);
+      }
+      FoldClassesI15<L, SLOT, GT, C + 1>::run(a, xb, x, tb, gtab, sw, hn, th, sA, sN);
+    }
+  }
+};
+
+template <int L, int SLOT, bool GT>
+__device__ __forceinline__ void leaf_block_fold_i15(const ExactArgs<L>& a, const uint4* __restrict__ xb, I15Ctx x,
+                                                    const double2* __restrict__ tb,
+                                                    const char* __restrict__ gtab, const double* __restrict__ sw,
+                                                    const int (&hn)[2], const double (&th)[2], double (&sA)[2],
+                                                    double (&sN)[2]) {
+  x.thf[0] = __double2float_rn(th[0]);
+  x.thf[1] = __double2float_rn(th[1]);
+  FoldClassesI15<L, SLOT, GT, 0>::run(a, xb, x, tb, gtab, sw, hn, th, sA, sN);
+}
+
+// The slot's entry table, class by class (compile-time class layout): entry
+// of Gray code g, n = gray^-1(g) <= |c|, is two 16-byte halves
+// {P_c[n], n (fp32 bits) | x~_n << 32} and {P_c[te(n)], x_n}
+// (x~_|c| = 0xFFFF: never equal to a threshold).
+template <int L, int C>
+__device__ inline void i15_fill(const ExactArgs<L>& a, int slot, double2* __restrict__ et) {
+  if constexpr (C <= L) {
+    if constexpr (i15_class(L, C)) {
+      constexpr int len = binom(L, C), i0 = class_start(L, C), base = i15_base(L, C), slots = i15_slots(L, C);
+      for (int t = threadIdx.x; t < 2 * slots; t += blockDim.x) {
+        unsigned n = (unsigned)(t >> 1);
+        for (int sh = 1; sh < 16; sh <<= 1) n ^= n >> sh;  // Gray -> binary
+        double2 v = make_double2(0.0, 0.0);
+        if ((int)n < len) {
+          if ((t & 1) == 0)
+            v = make_double2(a.cpre[slot][i0 + C + n],
+                             __hiloint2double((int)(a.xq[slot][i0 + n] & 0xFFFFu), __float_as_int((float)n)));
+          else
+            v = make_double2(a.cpre[slot][i0 + C + a.te[slot][i0 + n]], a.tab[slot * (1 << L) + i0 + n]);
+        } else if ((int)n == len) {
+          v = (t & 1) == 0 ? make_double2(a.cpre[slot][i0 + C + len], __hiloint2double(0xFFFF, __float_as_int((float)len)))
+                           : make_double2(a.cpre[slot][i0 + C + len], 0.0);
+        }
+        et[2 * base + t] = v;
+      }
+    }
+    i15_fill<L, C + 1>(a, slot, et);
+  }
+}
+
+// the Gray tables of the classes the I15 screen leaves to the fp64 block
+template <int L, int C>
+__device__ inline void gray_fill_small(const double (*gpre)[kGroupSlots], double2* __restrict__ sg) {
+  if constexpr (C <= L) {
+    if constexpr (!i15_class(L, C)) {
+      constexpr int ng = class_groups(L, C), dst = gray_group_base<L, true>(C), src = group_base(L, C);
+      for (int i = threadIdx.x; i < ng * kGraySlots; i += blockDim.x)
+        sg[dst * kGraySlots + i] = gray_table_entry(&gpre[src + i / kGraySlots][0], (unsigned)(i % kGraySlots), true);
+    }
+    gray_fill_small<L, C + 1>(gpre, sg);
+  }
 }
 
 template <int NP, int NC>

@@ -46,9 +46,23 @@ def test_table5_shared_sample_and_partitioned_ordering(study):
     # Theorem 1: partitioned (R per stratum) <= shared sample
     for M in part:
         assert part[M] <= shared[M] * 1.02, (M, part[M], shared[M])
-    # the published partitioned column at M = 1, 4, 8, 32, 64 (M = 2 and 16 are single-run outliers)
-    _check({M: part[M] for M in (1, 4, 8, 32, 64)},
-           {M: pt.PUBLISHED["table5_partitioned_var_asian"][M] for M in (1, 4, 8, 32, 64)}, rel=0.25)
+    # The published partitioned column is ONE run per cell.  Each cell is
+    # placed in the distribution of our 1000 single-run variance estimates:
+    # M = 1, 4, 8, 32, 64 lie inside its central 99 % (within the published
+    # rounding to 3 decimals); the published M = 2
+    # (0.220) and M = 16 (0.005) lie outside it (M = 2 above, M = 16 below; the
+    # bands are in profiles/r2_paper_tables_1000reps.json and DESIGN.md 3).
+    # The test pins exactly that: any other cell leaving the band fails.
+    pub = pt.PUBLISHED["table5_partitioned_var_asian"]
+    outside = {}
+    for M, v in pub.items():
+        lo, hi = study["table5_partitioned_var_asian_q"][M]
+        # the published value is rounded to 3 decimals: it stands for [v - 5e-4, v + 5e-4]
+        if v + 5e-4 < lo or v - 5e-4 > hi:
+            outside[M] = "above" if v - 5e-4 > hi else "below"
+    assert outside == {2: "above", 16: "below"}, outside
+    # where the published run sits inside the band, our mean tracks it within 25 %
+    _check({M: part[M] for M in (1, 4, 8, 32, 64)}, {M: pub[M] for M in (1, 4, 8, 32, 64)}, rel=0.25)
 
 
 def test_published_exact_values_within_4se():
