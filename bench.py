@@ -369,48 +369,84 @@ def fp64_peak(dev):
     return rate.value, mhz.value
 
 
-def roofline(w, workload, k_ms, paths, sm_count, clk, dev):
-    """FP64-pipe roofline of the dominant kernel (K1, with K2 inside k_ms).
+# Leaf-test forms of K1 and their peak rates per SM sub-partition per clock,
+# measured on this B200 (tools/microbench, profiles/r2_microbench_*.log):
+# any SETP (DSETP included) issues at 0.5 warp-instructions/clk -> 16 leaf
+# tests; the I15 screen's packed IMAD (two nodes' 15-bit lanes per 32-bit
+# lane) at 0.5 warp-instructions/clk -> 32 leaf tests.
+TESTS_PER_CLK_SMSP = {"fp64": 16.0, "i15": 32.0}
+I15_SHARE_L8 = 238.0 / 256.0  # leaves of the up-count classes with >= 16 leaves (L = 8): the screened ones
 
-    achieved = executed FP64-pipe ops per launch / kernel time, where the
-    executed ops per leaf test come from the committed ncu capture of this
-    instantiation (tools/ncu_opmix.py: DSETP + the per-group/per-node DFMA,
-    DADD, DMUL); a path has one leaf test per payoff.  peak = n_SM x 64 FP64
-    lanes x the SM clock seen during the timed region (nvidia-smi median;
-    K7's own clock when no sample exists) -- the FP64 pipe at the clock the
-    kernel ran at.  K7 (a DFMA microbenchmark) is reported beside it.
-    frac_w is the SURVEY §8d W-based figure (3 ops per path per payoff),
-    which can exceed 1 because K1 spends ~1.2 FP64 ops per leaf test."""
+
+def leaf_test_mix(kinds):
+    """(form, tests per path) of K1's leaf tests for the workload's kinds:
+    the Asian kinds screen their big classes (I15) and test the rest in fp64;
+    the lookback kinds test every leaf in fp64 (csrc/bp_exact_fast.cuh)."""
+    mix = {"fp64": 0.0, "i15": 0.0}
+    for k in kinds:
+        if k in ("asian-call", "asian-put"):
+            mix["i15"] += I15_SHARE_L8
+            mix["fp64"] += 1.0 - I15_SHARE_L8
+        else:
+            mix["fp64"] += 1.0
+    return mix
+
+
+def roofline(w, workload, k_ms, paths, sm_count, clk, dev):
+    """Compare roofline of the dominant kernel (K1, with K2 inside k_ms).
+
+    The algorithmic unit is the leaf test (one explicit compare per leaf per
+    payoff).  peak = the leaf-test rate of K1's own compare forms at their
+    measured pipe peak (TESTS_PER_CLK_SMSP), mixed in this workload's
+    proportions, x 4 sub-partitions x n_SM x the SM clock sampled during the
+    timed region; achieved = leaf tests per launch / kernel time; frac =
+    achieved / peak <= 1.  The ncu counters of the committed capture of this
+    instantiation (issue utilisation, warp instructions per leaf test, FP64
+    pipe) say where the rest of the time goes.  fp64_context keeps the
+    SURVEY §8d FP64-pipe figures: the W-based fraction (3 FP64 ops per path
+    per payoff, > 1 because K1 tests most leaves off the FP64 pipe) and the
+    K7 DFMA microbenchmark."""
     k7_rate, k7_mhz = fp64_peak(dev)
     mhz = (clk or {}).get("sm_mhz") or k7_mhz
-    peak = sm_count * FP64_LANES_PER_SM * mhz * 1e6
+    hz = mhz * 1e6
     tests = paths * len(w["kinds"])
-    c = load_counters(workload)
-    roof = {"bound": "fp64", "unit": "Tops/s (FP64 pipe)", "peak": peak / 1e12,
-            "peak_kind": f"{sm_count} SMs x {FP64_LANES_PER_SM} FP64 lanes x {mhz:.0f} MHz (SM clock sampled "
-                         "during the timed region)",
+    mix = leaf_test_mix(w["kinds"])
+    # seconds per path at the compare peak, per form
+    sec_per_path = sum(share / (TESTS_PER_CLK_SMSP[f] * 4 * sm_count * hz) for f, share in mix.items())
+    peak = len(w["kinds"]) / sec_per_path  # leaf tests / s
+    achieved = tests / (k_ms * 1e-3)
+    roof = {"bound": "compare", "unit": "leaf tests/s (x1e12)", "achieved": achieved / 1e12, "peak": peak / 1e12,
+            "frac": achieved / peak,
+            "peak_kind": (f"K1 leaf-test forms at their measured pipe peaks ({', '.join(f'{k} {v:g}' for k, v in TESTS_PER_CLK_SMSP.items())} "
+                          f"tests/clk/SMSP, profiles/r2_microbench_*.log) in this workload's mix "
+                          f"({', '.join(f'{k} {v:.3f}' for k, v in mix.items())} tests per path) x 4 x {sm_count} SMs "
+                          f"x {mhz:.0f} MHz (SM clock sampled during the timed region)"),
             "kernel_ms": k_ms, "paths_per_launch": paths, "leaf_tests_per_launch": tests}
+    c = load_counters(workload)
     if c:
-        ops = tests * c["fp64_pipe_ops_per_leaf_test"]
-        roof.update({"achieved": ops / (k_ms * 1e-3) / 1e12, "frac": ops / (k_ms * 1e-3) / peak,
-                     "traffic": c["dram_bytes_read"] + c["dram_bytes_write"],
+        roof.update({"traffic": c["dram_bytes_read"] + c["dram_bytes_write"],
                      "traffic_unit": "DRAM bytes per launch (ncu)",
-                     "fp64_ops_per_leaf_test": c["fp64_pipe_ops_per_leaf_test"],
-                     "ncu": {k: c[k] for k in ("fp64_pipe_active_pct", "issue_active_pct",
-                                               "warp_inst_per_32_leaf_tests", "fma_pipe_active_pct", "source")
+                     "ncu": {k: c[k] for k in ("issue_active_pct", "warp_inst_per_32_leaf_tests",
+                                               "fp64_pipe_active_pct", "alu_pipe_active_pct", "fma_pipe_active_pct",
+                                               "fp64_pipe_ops_per_leaf_test", "source")
                              if k in c}})
     else:
-        roof.update({"achieved": None, "frac": None, "traffic": None})
+        roof.update({"traffic": None})
+    fp64_peak_ops = sm_count * FP64_LANES_PER_SM * hz
     W = sum(W_OPS[k] for k in w["kinds"])
-    roof["frac_w"] = paths * W / (k_ms * 1e-3) / peak
-    roof["W_ops_per_path"] = W
-    roof["k7"] = {"dfma_per_s": k7_rate, "sm_mhz": k7_mhz,
-                  "frac_of_pipe_at_its_clock": k7_rate / (sm_count * FP64_LANES_PER_SM * k7_mhz * 1e6)
-                  if k7_mhz else None}
-    roof["fp32_context"] = {"peak_tflops": 2 * FP32_LANES_PER_SM * sm_count * mhz * 1e6 / 1e12,
-                            "note": "FMA-pipe peak at the same clock (FMA = 2 flops); the per-leaf test is an "
-                                    "FP64 compare, so K1 uses the FP32/FMA pipe only for integer address work "
-                                    "(ncu fma_pipe_active_pct)"}
+    roof["fp64_context"] = {
+        "peak_tops": fp64_peak_ops / 1e12,
+        "frac_w": paths * W / (k_ms * 1e-3) / fp64_peak_ops, "W_ops_per_path": W,
+        "note": "SURVEY 8d W-based FP64 figure: 3 FP64 ops per path per payoff over the FP64-pipe peak "
+                f"({sm_count} SMs x {FP64_LANES_PER_SM} lanes x {mhz:.0f} MHz); above 1 because K1 screens most "
+                "leaves with 15-bit integer compares and spends FP64 only on the lookback leaves, the small "
+                "classes and the ambiguous boundary leaf",
+        "k7": {"dfma_per_s": k7_rate, "sm_mhz": k7_mhz,
+               "frac_of_pipe_at_its_clock": k7_rate / (sm_count * FP64_LANES_PER_SM * k7_mhz * 1e6)
+               if k7_mhz else None}}
+    roof["fp32_context"] = {"peak_tflops": 2 * FP32_LANES_PER_SM * sm_count * hz / 1e12,
+                            "note": "FMA-pipe peak at the same clock (FMA = 2 flops); the screen's packed IMAD runs "
+                                    "on the FMA pipe (ncu fma_pipe_active_pct)"}
     return roof
 
 
@@ -561,8 +597,11 @@ def run_ours(args):
         "impl_detail": {"parallelism": f"superblock-shard x{world} (one rank per GPU, NCCL all_gather)",
                         "l2": "flushed (256 MiB write) between timed steps",
                         "engine": "affine-threshold" if sh.engine else "path-walk", "inner_bits": sh.inner_bits,
-                        "superblocks": sh.n_sb, "leaf_block": "Gray-code predicate counting, per-class fold, "
-                                                             "2 nodes per table load"},
+                        "superblocks": sh.n_sb, "leaf_block": "Asian kinds: 15-bit integer screen of the "
+                                                             "big classes (two nodes per IMAD, Gray-code counters, "
+                                                             "fp64 boundary leaf); lookback kinds and small classes: "
+                                                             "fp64 compares with Gray-code predicate counting; "
+                                                             "per-class fold, 2 nodes per table load"},
         "values": vals, "config3": extra or None, **extra45, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clocks,

@@ -41,8 +41,13 @@ __host__ __device__ constexpr int fast_tables(unsigned km) {
 #ifndef BP_MINB2
 #define BP_MINB2 2  // ... and by the fused two-table kernels
 #endif
+#ifndef BP_MINB_I15
+#define BP_MINB_I15 3  // ... and by the one-table kernels of the Asian kinds (I15 screen)
+#endif
 template <int L, unsigned KM, bool CNT>
-__global__ void __launch_bounds__(256, fast_tables(KM) == 2 ? BP_MINB2 : BP_MINB1)
+__global__ void __launch_bounds__(256, fast_tables(KM) == 2                                      ? BP_MINB2
+                                       : (i15_on<L>() && (KM & ((1u << kAC) | (1u << kAP))))     ? BP_MINB_I15
+                                                                                                 : BP_MINB1)
 k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_out,
              unsigned long long* __restrict__ hist) {
   constexpr int NC = L + 1;
@@ -66,7 +71,10 @@ k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_
   // fp64 block): its entry tables, screened values and tie-run ends, and the
   // Gray tables of the classes it leaves to the fp64 block; the other slot
   // keeps all its Gray tables
-  constexpr bool I15 = i15_on<L>() && (kAC_ || kAP_);
+#ifndef BP_I15_LOOKBACK
+#define BP_I15_LOOKBACK 0  // diagnostics: 1 = the screen on the lookback slot too (r2 scan: no gain)
+#endif
+  constexpr bool I15 = i15_on<L>() && (kAC_ || kAP_ || (BP_I15_LOOKBACK && NT == 1));
   constexpr int NG0 = I15 ? n_small_groups<L>() : NG;
   __shared__ __align__(16) double2 sgray0[NT > 0 ? NG0 * kGraySlots : 1];
   __shared__ __align__(16) double2 sgray1[NT > 1 ? NG * kGraySlots : 1];

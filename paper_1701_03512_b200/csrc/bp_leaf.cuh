@@ -240,6 +240,10 @@ struct I15Ctx {
   float thf[2];         // node thresholds in fp32
 };
 constexpr int kI15Entry = 32;  // bytes per entry
+#ifndef BP_I15_WAYS
+#define BP_I15_WAYS 1  // r2 scan: 1 (no partials) best at 3 CTAs/SM, equal at 2
+#endif
+constexpr int kI15Ways = BP_I15_WAYS;  // partial Gray counters per bit
 
 __host__ __device__ constexpr int ctz_c(int v) {
   int b = 0;
@@ -255,9 +259,13 @@ struct I15Class {
     const float s = a.nrm_s[SLOT][C], o = a.nrm_o[SLOT][C];
     const unsigned k0 = i15_map(x.thf[0], s, o), k1 = i15_map(x.thf[1], s, o);
     const unsigned T = __byte_perm(0x7FFFu - k0, 0x7FFFu - k1, 0x5410);
-    unsigned g[nb];
+    // counter bit b collects leaves j = 2^b - 1 + 2^(b+1) t; kI15Ways partial
+    // counters per bit (by t) keep the XOR dependency chains short
+    unsigned gp[nb][kI15Ways];
 #pragma unroll
-    for (int b = 0; b < nb; ++b) g[b] = 0u;
+    for (int b = 0; b < nb; ++b)
+#pragma unroll
+      for (int q = 0; q < kI15Ways; ++q) gp[b][q] = 0u;
 #pragma unroll
     for (int j = 0; j < len; ++j) {
       const uint4 w = xb[(i0 + j) >> 2];
@@ -265,7 +273,15 @@ struct I15Class {
       const unsigned xv = r == 0 ? w.x : r == 1 ? w.y : r == 2 ? w.z : w.w;
       unsigned d;
       asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(xv), "r"(x.one), "r"(T));
-      g[ctz_c(j + 1)] ^= d;
+      const int b = ctz_c(j + 1);
+      gp[b][((j + 1) >> (b + 1)) % kI15Ways] ^= d;
+    }
+    unsigned g[nb];
+#pragma unroll
+    for (int b = 0; b < nb; ++b) {
+      g[b] = gp[b][0];
+#pragma unroll
+      for (int q = 1; q < kI15Ways; ++q) g[b] ^= gp[b][q];
     }
     // byte offsets of the two lanes' codes: lane 1's bits (bit 31 of each
     // counter) shift in from the top, lane 0's (bit 15) are masked and added

@@ -40,6 +40,7 @@ def main():
         "fp64_pipe_active_pct": num("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"),
         "issue_active_pct": num("smsp__issue_active.avg.pct_of_peak_sustained_active"),
         "fma_pipe_active_pct": num("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"),
+        "alu_pipe_active_pct": num("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
         "warp_inst_per_32_leaf_tests": sum(agg.values()) * per,
         "fp64_pipe_ops_per_leaf_test": fp64 * per,
         "local_loads": num("smsp__sass_inst_executed_op_local_ld.sum"),

@@ -14,6 +14,8 @@ reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 wl, classic_crr = bench.workloads()
 if name == "N30ac":
     w = dict(wl["config2"], kinds=["asian-call"])
+elif name == "N30fl":
+    w = dict(wl["config2"], kinds=["float-lookback"])
 elif name == "N32ac":
     w = dict(wl["config2"], N=32, kinds=["asian-call"])
 else:
