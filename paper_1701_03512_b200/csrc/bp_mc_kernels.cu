@@ -163,64 +163,61 @@ __device__ __forceinline__ PathState walk_suffix(const McArgs& a, const Nib* __r
   return st;
 }
 
-// Two independent draws walked in lock step (the Philox rounds of the two
+// NS independent draws walked in lock step (the Philox rounds of the NS
 // counters interleave, giving the scheduler independent work) -- same bits
 // and same arithmetic per draw as walk_suffix.
-template <unsigned KIND, bool CONSTP>
-__device__ __forceinline__ void walk_suffix2(const McArgs& a, const Nib* __restrict__ nib, PathState& s0,
-                                             PathState& s1, uint32_t i0, uint32_t i1, uint32_t stream, uint32_t rep,
-                                             uint32_t thr0, bool all_up) {
+template <unsigned KIND, bool CONSTP, int NS>
+__device__ __forceinline__ void walk_suffix_n(const McArgs& a, const Nib* __restrict__ nib, PathState (&s)[NS],
+                                              uint32_t i0, uint32_t stride, uint32_t stream, uint32_t rep,
+                                              uint32_t thr0, bool all_up) {
   constexpr bool need_max = KIND == kFL;
   constexpr bool need_min = KIND == kFLP;
   constexpr bool need_sum = KIND == kAC || KIND == kAP;
   const int nsuf = a.N - a.r;
   const int nfull = nsuf >> 2;
-  uint32_t b0[4], b1[4];
+  uint32_t blk[NS][4];
   auto up_of = [&](int w, uint32_t word) -> bool {
     if (CONSTP) return (word < thr0) || all_up;
     const int t = a.r + w;
     return (word < a.thr[t]) || ((t < 32 ? (a.always[0] >> t) : (a.always[1] >> (t - 32))) & 1u);
   };
-  auto step4 = [&](PathState& st, const uint32_t (&blk)[4], int j) {
-    const unsigned b = ((unsigned)up_of(4 * j, blk[0]) << 3) | ((unsigned)up_of(4 * j + 1, blk[1]) << 2) |
-                       ((unsigned)up_of(4 * j + 2, blk[2]) << 1) | (unsigned)up_of(4 * j + 3, blk[3]);
-    const Nib q = nib[b];
-    if (need_sum) st.sum = fma(st.S, q.c, st.sum);
-    if (need_max) st.mx = fmax(st.mx, st.S * q.x);
-    if (need_min) st.mn = fmin(st.mn, st.S * q.n);
-    st.S *= q.e;
-  };
   for (int j = 0; j < nfull; ++j) {
-    philox4x32_10((uint32_t)j, i0, stream, rep, a.key0, a.key1, b0);
-    philox4x32_10((uint32_t)j, i1, stream, rep, a.key0, a.key1, b1);
-    step4(s0, b0, j);
-    step4(s1, b1, j);
+#pragma unroll
+    for (int d = 0; d < NS; ++d) philox4x32_10((uint32_t)j, i0 + d * stride, stream, rep, a.key0, a.key1, blk[d]);
+#pragma unroll
+    for (int d = 0; d < NS; ++d) {
+      const unsigned b = ((unsigned)up_of(4 * j, blk[d][0]) << 3) | ((unsigned)up_of(4 * j + 1, blk[d][1]) << 2) |
+                         ((unsigned)up_of(4 * j + 2, blk[d][2]) << 1) | (unsigned)up_of(4 * j + 3, blk[d][3]);
+      const Nib q = nib[b];
+      if (need_sum) s[d].sum = fma(s[d].S, q.c, s[d].sum);
+      if (need_max) s[d].mx = fmax(s[d].mx, s[d].S * q.x);
+      if (need_min) s[d].mn = fmin(s[d].mn, s[d].S * q.n);
+      s[d].S *= q.e;
+    }
   }
   if (4 * nfull < nsuf) {
-    philox4x32_10((uint32_t)nfull, i0, stream, rep, a.key0, a.key1, b0);
-    philox4x32_10((uint32_t)nfull, i1, stream, rep, a.key0, a.key1, b1);
+#pragma unroll
+    for (int d = 0; d < NS; ++d) philox4x32_10((uint32_t)nfull, i0 + d * stride, stream, rep, a.key0, a.key1, blk[d]);
 #pragma unroll
     for (int l = 0; l < 3; ++l) {
       const int w = 4 * nfull + l;
       if (w < nsuf) {
-        s0.S *= up_of(w, b0[l]) ? a.u : a.d;
-        s1.S *= up_of(w, b1[l]) ? a.u : a.d;
-        if (need_sum) {
-          s0.sum += s0.S;
-          s1.sum += s1.S;
-        }
-        if (need_max) {
-          s0.mx = fmax(s0.mx, s0.S);
-          s1.mx = fmax(s1.mx, s1.S);
-        }
-        if (need_min) {
-          s0.mn = fmin(s0.mn, s0.S);
-          s1.mn = fmin(s1.mn, s1.S);
+#pragma unroll
+        for (int d = 0; d < NS; ++d) {
+          s[d].S *= up_of(w, blk[d][l]) ? a.u : a.d;
+          if (need_sum) s[d].sum += s[d].S;
+          if (need_max) s[d].mx = fmax(s[d].mx, s[d].S);
+          if (need_min) s[d].mn = fmin(s[d].mn, s[d].S);
         }
       }
     }
   }
 }
+
+#ifndef BP_MC_NS
+#define BP_MC_NS 2  // draws per thread in lock step (K4; r2 scan: 2, 4, 8 within 1 %)
+#endif
+constexpr int kMcNS = BP_MC_NS;
 
 // Per-thread running statistics without a per-draw division: sums of
 // (v - c) and (v - c)^2 around the thread's first value c (no cancellation
@@ -263,14 +260,24 @@ k_mc_strata(const __grid_constant__ McArgs a, const unsigned long long* __restri
     const PathState pre = prefix_state(a, m);
     ShiftedSums acc{0.0, 0.0, 0.0, 0.0};
     unsigned long long i = first + threadIdx.x;
-    // pairs of draws (i, i + 256) in lock step, then a possible single tail draw;
-    // values are added in ascending draw order, as the one-at-a-time loop did
-    for (; i + kMcThreads < last; i += 2 * kMcThreads) {
-      PathState s0 = pre, s1 = pre;
-      walk_suffix2<KIND, CONSTP>(a, nib, s0, s1, (uint32_t)i, (uint32_t)(i + kMcThreads), (uint32_t)m,
-                                 a.rep0 + (uint32_t)k, thr0, all_up);
-      acc.add(payoff_of(KIND, s0, a.K, a.N));
-      acc.add(payoff_of(KIND, s1, a.K, a.N));
+    // groups of kMcNS draws (i, i + 256, ...) in lock step, then pairs, then a
+    // possible single tail draw; values are added in ascending draw order, as
+    // the one-at-a-time loop did
+    for (; i + (kMcNS - 1) * kMcThreads < last; i += kMcNS * kMcThreads) {
+      PathState sd[kMcNS];
+#pragma unroll
+      for (int d = 0; d < kMcNS; ++d) sd[d] = pre;
+      walk_suffix_n<KIND, CONSTP, kMcNS>(a, nib, sd, (uint32_t)i, kMcThreads, (uint32_t)m, a.rep0 + (uint32_t)k,
+                                         thr0, all_up);
+#pragma unroll
+      for (int d = 0; d < kMcNS; ++d) acc.add(payoff_of(KIND, sd[d], a.K, a.N));
+    }
+    for (; kMcNS > 2 && i + kMcThreads < last; i += 2 * kMcThreads) {
+      PathState sd[2] = {pre, pre};
+      walk_suffix_n<KIND, CONSTP, 2>(a, nib, sd, (uint32_t)i, kMcThreads, (uint32_t)m, a.rep0 + (uint32_t)k, thr0,
+                                     all_up);
+      acc.add(payoff_of(KIND, sd[0], a.K, a.N));
+      acc.add(payoff_of(KIND, sd[1], a.K, a.N));
     }
     if (i < last) {
       const PathState st = walk_suffix<KIND, CONSTP>(a, nib, pre, (uint32_t)i, (uint32_t)m, a.rep0 + (uint32_t)k, thr0,
