@@ -1188,10 +1188,14 @@ static void run_device_job(const bp_tree* t, uint32_t payoffs, uint32_t flags, D
   if (!rc && try_graph_job(c, P, job, flags, cnt)) {  // class engine, repeated valuation: one graph launch
     const auto t2 = clk::now();
     if ((e = cudaStreamSynchronize(c.st)) != cudaSuccess) return cuda_fail(e, "valuation (graph)");
-    if (trace)
-      std::fprintf(stderr, "[bp trace] dev %d: plan %.1f us, graph launch %.1f us\n", job->device,
-                   std::chrono::duration<double, std::micro>(t1 - t0).count(),
-                   std::chrono::duration<double, std::micro>(t2 - t1).count());
+    if (trace) {
+      float gms = 0.f;
+      cudaEventElapsedTime(&gms, c.e0, c.e1);
+      std::fprintf(stderr, "[bp trace] dev %d: plan %.1f us, graph key + launch %.1f us, wait %.1f us (device %.1f us)\n",
+                   job->device, std::chrono::duration<double, std::micro>(t1 - t0).count(),
+                   std::chrono::duration<double, std::micro>(t2 - t1).count(),
+                   std::chrono::duration<double, std::micro>(clk::now() - t2).count(), gms * 1e3);
+    }
     std::memcpy(job->partials.data(), c.out_host, sizeof(double) * np);
     cudaEventElapsedTime(&job->ms, c.e0, c.e1);
     return;
@@ -1232,6 +1236,7 @@ static void run_device_job(const bp_tree* t, uint32_t payoffs, uint32_t flags, D
 
 extern "C" int bp_exact(const bp_tree* tree, uint32_t payoffs, uint32_t flags, int n_dev, const int* devices,
                         bp_exact_result* out) {
+  const auto tb0 = std::chrono::steady_clock::now();
   int rc = validate_tree(tree, 62, true);
   if (rc) return rc;
   if ((rc = kinds_ok(payoffs))) return rc;
@@ -1256,8 +1261,13 @@ extern "C" int bp_exact(const bp_tree* tree, uint32_t payoffs, uint32_t flags, i
     jobs[g].sb_count = cnt;
     first += cnt;
   }
+  const auto tb1 = std::chrono::steady_clock::now();
   if (G == 1) {
     run_device_job(tree, payoffs, flags, &jobs[0]);
+    if (trace_on())
+      std::fprintf(stderr, "[bp trace] bp_exact: validate + layout %.1f us, device job %.1f us\n",
+                   std::chrono::duration<double, std::micro>(tb1 - tb0).count(),
+                   std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - tb1).count());
   } else {
     std::vector<std::thread> th;
     for (int g = 0; g < G; ++g) th.emplace_back(run_device_job, tree, payoffs, flags, &jobs[g]);
