@@ -42,7 +42,16 @@ k_exact_batch(const BatchOption* __restrict__ opts, BatchArgs ba, double2* __res
   constexpr bool DESC = AC || FL;  // compare direction '>' -> sort descending
   __shared__ __align__(16) double tab[NL];
   __shared__ double gpre[NG * kGroupSlots];
-  __shared__ __align__(16) double2 sgray[TAB ? NG * kGraySlots : 1];
+  // I15 screen (Asian kinds, as K1): the big classes' screen tables, built per
+  // CTA from the option's sorted table; Gray tables only for the small classes
+  constexpr bool I15 = (AC || AP) && i15_on<kBL>();
+  constexpr int NGG = I15 ? n_small_groups<kBL>() : NG;
+  __shared__ __align__(16) double2 sgray[TAB ? NGG * kGraySlots : 1];
+  __shared__ float i15_s[I15 ? NC : 1], i15_o[I15 ? NC : 1];
+  __shared__ double i15_cpre[I15 ? NL + NC : 1];
+  __shared__ __align__(16) unsigned i15_xq[I15 ? NL : 4];
+  __shared__ unsigned char i15_te[I15 ? NL : 4];
+  __shared__ __align__(16) double2 i15_et[I15 ? 2 * i15_entries(kBL) : 1];
   __shared__ double sW1[(FL || FLP) ? kMaxN + 2 : 1], sW2[(FL || FLP) ? kMaxN + 2 : 1];
   __shared__ double mid_c[NMID], mid_e[NMID], mid_x[NMID];
   __shared__ int mid_h[NMID];
@@ -142,9 +151,53 @@ k_exact_batch(const BatchOption* __restrict__ opts, BatchArgs ba, double2* __res
     }
   __syncthreads();
   // Gray-ordered {prefix sum, count} tables (count as a double: the fold form)
-  if (TAB)
+  if constexpr (I15) {
+    gray_fill_small<kBL, 0>(reinterpret_cast<const double(*)[kGroupSlots]>(gpre), sgray);
+    // per big class (one thread each): the monotone map onto [4, 32763] (as
+    // the host builds it for K1, i15_layout) and the class prefix sums
+    if (tid < NC && i15_class(kBL, tid)) {
+      const int c = tid, i0 = class_start(kBL, c), len = binom(kBL, c);
+      float lo = (float)tab[i0], hi = lo;
+      for (int k = 0; k < len; ++k) {
+        lo = fminf(lo, (float)tab[i0 + k]);
+        hi = fmaxf(hi, (float)tab[i0 + k]);
+      }
+      const float range = hi - lo, amax = fmaxf(fabsf(lo), fabsf(hi));
+      double sc = range > 0.0f ? 32759.0 / (double)range : 1.0;
+      if (amax > 0.0f) sc = fmin(sc, 4194304.0 / (double)amax);
+      if (!(sc > 0.0) || !isfinite(sc)) sc = 1.0;
+      const float sf = (float)(DESC ? sc : -sc);
+      const double off = (double)kI15Magic + 4.0 - (double)(DESC ? lo : hi) * (double)sf;
+      i15_s[c] = sf;
+      i15_o[c] = isfinite(off) ? (float)off : kI15Magic;
+      double sum = 0.0, comp = 0.0;
+      i15_cpre[i0 + c] = 0.0;
+      for (int k = 0; k < len; ++k) {
+        comp_add(sum, comp, tab[i0 + k]);
+        i15_cpre[i0 + c + k + 1] = sum + comp;
+      }
+    }
+    __syncthreads();
+    // per position: the screened value in both lanes and the tie-run end
+    if (tid < NL) {
+      int c = 0;
+      while (tid >= class_start(kBL, c + 1)) ++c;
+      if (i15_class(kBL, c)) {
+        const int i0 = class_start(kBL, c), len = binom(kBL, c);
+        const unsigned k = i15_map((float)tab[tid], i15_s[c], i15_o[c]);
+        i15_xq[tid] = k | (k << 16);
+        const double tol = ldexp(fabs(tab[tid]), -44);
+        int e = tid - i0 + 1;
+        while (e < len && fabs(tab[i0 + e] - tab[tid]) <= tol) ++e;
+        i15_te[tid] = (unsigned char)e;
+      }
+    }
+    __syncthreads();
+    i15_fill<kBL, 0>(SmemTabs{i15_s, i15_o, tab, i15_cpre, i15_xq, i15_te}, i15_et);
+  } else if (TAB) {
     for (int i = tid; i < NG * kGraySlots; i += kBThreads)
       sgray[i] = gray_table_entry(&gpre[(i / kGraySlots) * kGroupSlots], (unsigned)(i % kGraySlots), true);
+  }
   __syncthreads();
 
   const double NK = (double)N * o.K;
@@ -183,8 +236,16 @@ k_exact_batch(const BatchOption* __restrict__ opts, BatchArgs ba, double2* __res
         // node value, affine in sA = sum_c w[h+c] A_c and sN = sum_c w[h+c] n_c
         // (the K1 fold forms, bp_exact_fast.cuh)
         double sA[NP], sN[NP];
-        leaf_block_fold<kBL, NP, 0, DESC>(reinterpret_cast<const double2*>(tab) + (j0 & zero),
-                                          reinterpret_cast<const char*>(sgray), w, hn, th, sA, sN);
+        if constexpr (I15)
+          leaf_block_fold_i15<kBL, 0, DESC>(SmemTabs{i15_s, i15_o, tab, i15_cpre, i15_xq, i15_te},
+                                            reinterpret_cast<const uint4*>(i15_xq) + (j0 & zero),
+                                            I15Ctx{reinterpret_cast<const char*>(i15_et), i15_xq, i15_te,
+                                                   1u | (unsigned)zero, {0.f, 0.f}},
+                                            reinterpret_cast<const double2*>(tab) + (j0 & zero),
+                                            reinterpret_cast<const char*>(sgray), w, hn, th, sA, sN);
+        else
+          leaf_block_fold<kBL, NP, 0, DESC>(reinterpret_cast<const double2*>(tab) + (j0 & zero),
+                                            reinterpret_cast<const char*>(sgray), w, hn, th, sA, sN);
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
           double val;

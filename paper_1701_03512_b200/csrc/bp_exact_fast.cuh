@@ -83,7 +83,7 @@ k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_
   __shared__ unsigned char ste[I15 ? (1 << L) : 4];
   if constexpr (I15) {
     gray_fill_small<L, 0>(a.gpre[0], sgray0);
-    i15_fill<L, 0>(a, 0, si15);
+    i15_fill<L, 0>(ParamTabs<L, 0>{a}, si15);
     for (int i = threadIdx.x; i < (1 << L); i += blockDim.x) {
       sxq[i] = a.xq[0][i];
       ste[i] = a.te[0][i];
@@ -190,7 +190,7 @@ k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_
       // the leaf block of a slot: I15 screen on slot 0 of the Asian kinds
 #define BP_FOLDLEAF(SLOT, GTV, TH)                                                                            \
   if constexpr (I15 && (SLOT) == 0)                                                                          \
-    leaf_block_fold_i15<L, SLOT, GTV>(a, reinterpret_cast<const uint4*>(sxq) + zoff,                        \
+    leaf_block_fold_i15<L, SLOT, GTV>(ParamTabs<L, SLOT>{a}, reinterpret_cast<const uint4*>(sxq) + zoff,    \
                                       I15Ctx{reinterpret_cast<const char*>(si15), sxq, ste,                  \
                                              1u | (unsigned)sc.zero, {0.f, 0.f}},                           \
                                       tb, BP_GTAB(SLOT), sw, hn, TH, sA, sN);                                \

@@ -251,12 +251,38 @@ __host__ __device__ constexpr int ctz_c(int v) {
   return b;
 }
 
-template <int L, int SLOT, bool GT, int C>
+// Where a slot's screen tables live: the kernel parameter block (K1: uniform
+// constant-bank loads at compile-time offsets) or shared memory (K3: built by
+// each CTA for its option).  i = class-major position, slot-relative.
+template <int L, int SLOT>
+struct ParamTabs {
+  const ExactArgs<L>& a;
+  __device__ __forceinline__ float nrm_s(int c) const { return a.nrm_s[SLOT][c]; }
+  __device__ __forceinline__ float nrm_o(int c) const { return a.nrm_o[SLOT][c]; }
+  __device__ __forceinline__ double tab(int i) const { return a.tab[SLOT * (1 << L) + i]; }
+  __device__ __forceinline__ double cpre(int i) const { return a.cpre[SLOT][i]; }
+  __device__ __forceinline__ unsigned xq(int i) const { return a.xq[SLOT][i]; }
+  __device__ __forceinline__ unsigned te(int i) const { return a.te[SLOT][i]; }
+};
+struct SmemTabs {
+  const float *ns, *no;
+  const double *tb, *cp;
+  const unsigned* xw;
+  const unsigned char* tw;
+  __device__ __forceinline__ float nrm_s(int c) const { return ns[c]; }
+  __device__ __forceinline__ float nrm_o(int c) const { return no[c]; }
+  __device__ __forceinline__ double tab(int i) const { return tb[i]; }
+  __device__ __forceinline__ double cpre(int i) const { return cp[i]; }
+  __device__ __forceinline__ unsigned xq(int i) const { return xw[i]; }
+  __device__ __forceinline__ unsigned te(int i) const { return tw[i]; }
+};
+
+template <int L, int SLOT, bool GT, int C, class TS>
 struct I15Class {
   static constexpr int len = binom(L, C), nb = bit_length(len), i0 = class_start(L, C);
-  static __device__ __forceinline__ void run(const ExactArgs<L>& a, const uint4* __restrict__ xb, const I15Ctx& x,
+  static __device__ __forceinline__ void run(const TS& a, const uint4* __restrict__ xb, const I15Ctx& x,
                                              const double (&th)[2], double (&A)[2], double (&n)[2]) {
-    const float s = a.nrm_s[SLOT][C], o = a.nrm_o[SLOT][C];
+    const float s = a.nrm_s(C), o = a.nrm_o(C);
     const unsigned k0 = i15_map(x.thf[0], s, o), k1 = i15_map(x.thf[1], s, o);
     const unsigned T = __byte_perm(0x7FFFu - k0, 0x7FFFu - k1, 0x5410);
     // counter bit b collects leaves j = 2^b - 1 + 2^(b+1) t; kI15Ways partial
@@ -297,8 +323,9 @@ struct I15Class {
     double2 r0 = make_double2(e0.x, (double)__int_as_float(__double2loint(e0.y)));
     double2 r1 = make_double2(e1.x, (double)__int_as_float(__double2loint(e1.y)));
     const bool amb0 = (unsigned)__double2hiint(e0.y) == k0, amb1 = (unsigned)__double2hiint(e1.y) == k1;
-    // warp-uniform branch (the surrounding control flow stays uniform)
-    if (__any_sync(0xffffffffu, amb0 || amb1)) {
+    // warp-uniform branch (the surrounding control flow stays uniform; K3 may
+    // run partial warps on tiny trees, hence the active mask)
+    if (__any_sync(__activemask(), amb0 || amb1)) {
       fix(a, x, et0, th[0], k0, amb0, r0);
       fix(a, x, et1, th[1], k1, amb1, r1);
     }
@@ -309,7 +336,7 @@ struct I15Class {
   }
   // leaf n' in fp64 from the entry (with its tie run); a further leaf with
   // the threshold's screened value takes the exact walk
-  static __device__ __forceinline__ void fix(const ExactArgs<L>& a, const I15Ctx& x, const char* et, double th,
+  static __device__ __forceinline__ void fix(const TS& a, const I15Ctx& x, const char* et, double th,
                                              unsigned k, bool amb, double2& r) {
     if (!amb) return;
     const double2 e1 = *reinterpret_cast<const double2*>(et + 16);  // {P_c[m], x_n'}
@@ -319,28 +346,28 @@ struct I15Class {
       if (m < len && (x.sxq[i0 + m] & 0xFFFFu) == k) r = walk(a, x, th, k, m);
     }
   }
-  static __device__ __noinline__ double2 walk(const ExactArgs<L>& a, const I15Ctx& x, double th, unsigned k, int j) {
+  static __device__ __noinline__ double2 walk(const TS& a, const I15Ctx& x, double th, unsigned k, int j) {
     while (j < len && (x.sxq[i0 + j] & 0xFFFFu) == k) {
-      const double v = a.tab[SLOT * (1 << L) + i0 + j];
+      const double v = a.tab(i0 + j);
       if (!(GT ? v > th : v < th)) break;
       j = x.ste[i0 + j];
     }
-    return make_double2(a.cpre[SLOT][i0 + C + j], (double)j);
+    return make_double2(a.cpre(i0 + C + j), (double)j);
   }
 };
 
 // K1 leaf block with the I15 screen on the big classes and the Gray fp64
 // block (FoldGroups) on the others; per class the fold as leaf_block_fold.
-template <int L, int SLOT, bool GT, int C>
+template <int L, int SLOT, bool GT, int C, class TS>
 struct FoldClassesI15 {
-  static __device__ __forceinline__ void run(const ExactArgs<L>& a, const uint4* __restrict__ xb, const I15Ctx& x,
+  static __device__ __forceinline__ void run(const TS& a, const uint4* __restrict__ xb, const I15Ctx& x,
                                              const double2* __restrict__ tb, const char* __restrict__ gtab,
                                              const double* __restrict__ sw, const int (&hn)[2],
                                              const double (&th)[2], double (&sA)[2], double (&sN)[2]) {
     if constexpr (C <= L) {
       double A[2], n[2];
       if constexpr (i15_class(L, C))
-        I15Class<L, SLOT, GT, C>::run(a, xb, x, th, A, n);
+        I15Class<L, SLOT, GT, C, TS>::run(a, xb, x, th, A, n);
       else
         FoldGroups<L, 2, SLOT, GT, C, 0, true>::run(tb, gtab, th, A, n);
 #pragma unroll
@@ -349,28 +376,28 @@ struct FoldClassesI15 {
         sA[p] = C == 0 ? w * A[p] : fma(w, A[p], sA[p]);
         sN[p] = C == 0 ? w * n[p] : fma(w, n[p], sN[p]);
       }
-      FoldClassesI15<L, SLOT, GT, C + 1>::run(a, xb, x, tb, gtab, sw, hn, th, sA, sN);
+      FoldClassesI15<L, SLOT, GT, C + 1, TS>::run(a, xb, x, tb, gtab, sw, hn, th, sA, sN);
     }
   }
 };
 
-template <int L, int SLOT, bool GT>
-__device__ __forceinline__ void leaf_block_fold_i15(const ExactArgs<L>& a, const uint4* __restrict__ xb, I15Ctx x,
+template <int L, int SLOT, bool GT, class TS>
+__device__ __forceinline__ void leaf_block_fold_i15(const TS& a, const uint4* __restrict__ xb, I15Ctx x,
                                                     const double2* __restrict__ tb,
                                                     const char* __restrict__ gtab, const double* __restrict__ sw,
                                                     const int (&hn)[2], const double (&th)[2], double (&sA)[2],
                                                     double (&sN)[2]) {
   x.thf[0] = __double2float_rn(th[0]);
   x.thf[1] = __double2float_rn(th[1]);
-  FoldClassesI15<L, SLOT, GT, 0>::run(a, xb, x, tb, gtab, sw, hn, th, sA, sN);
+  FoldClassesI15<L, SLOT, GT, 0, TS>::run(a, xb, x, tb, gtab, sw, hn, th, sA, sN);
 }
 
 // The slot's entry table, class by class (compile-time class layout): entry
 // of Gray code g, n = gray^-1(g) <= |c|, is two 16-byte halves
 // {P_c[n], n (fp32 bits) | x~_n << 32} and {P_c[te(n)], x_n}
 // (x~_|c| = 0xFFFF: never equal to a threshold).
-template <int L, int C>
-__device__ inline void i15_fill(const ExactArgs<L>& a, int slot, double2* __restrict__ et) {
+template <int L, int C, class TS>
+__device__ inline void i15_fill(const TS& a, double2* __restrict__ et) {
   if constexpr (C <= L) {
     if constexpr (i15_class(L, C)) {
       constexpr int len = binom(L, C), i0 = class_start(L, C), base = i15_base(L, C), slots = i15_slots(L, C);
@@ -380,18 +407,18 @@ __device__ inline void i15_fill(const ExactArgs<L>& a, int slot, double2* __rest
         double2 v = make_double2(0.0, 0.0);
         if ((int)n < len) {
           if ((t & 1) == 0)
-            v = make_double2(a.cpre[slot][i0 + C + n],
-                             __hiloint2double((int)(a.xq[slot][i0 + n] & 0xFFFFu), __float_as_int((float)n)));
+            v = make_double2(a.cpre(i0 + C + n),
+                             __hiloint2double((int)(a.xq(i0 + n) & 0xFFFFu), __float_as_int((float)n)));
           else
-            v = make_double2(a.cpre[slot][i0 + C + a.te[slot][i0 + n]], a.tab[slot * (1 << L) + i0 + n]);
+            v = make_double2(a.cpre(i0 + C + a.te(i0 + n)), a.tab(i0 + n));
         } else if ((int)n == len) {
-          v = (t & 1) == 0 ? make_double2(a.cpre[slot][i0 + C + len], __hiloint2double(0xFFFF, __float_as_int((float)len)))
-                           : make_double2(a.cpre[slot][i0 + C + len], 0.0);
+          v = (t & 1) == 0 ? make_double2(a.cpre(i0 + C + len), __hiloint2double(0xFFFF, __float_as_int((float)len)))
+                           : make_double2(a.cpre(i0 + C + len), 0.0);
         }
         et[2 * base + t] = v;
       }
     }
-    i15_fill<L, C + 1>(a, slot, et);
+    i15_fill<L, C + 1, TS>(a, et);
   }
 }
 
