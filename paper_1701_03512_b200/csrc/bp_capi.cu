@@ -22,6 +22,7 @@
 #include "../../include/binpaths_b200.h"
 #include "bp_exact.cuh"
 #include "bp_kernels.h"
+#include "bp_leaf.cuh"  // gray_table_entry (K1 shared-memory image)
 #include "bp_threshold.h"
 #include "bp_exact_w.cuh"
 
@@ -307,6 +308,76 @@ static void i15_layout(int kind, const double* pos, ExactArgs<L>& a, int slot) {
   }
 }
 
+// K1's shared-memory image (k1_smem_layout), appended to the argument block:
+// the tables every CTA used to build from the parameter bank, built once here
+// with the same formulas (kernel fallback: bp_exact_fast.cuh, ga == nullptr).
+template <int L>
+static void build_smem_image(const ExactArgs<L>& a, unsigned km, unsigned char* img) {
+  const K1SmemLayout ly = k1_smem_layout<L>(km);
+  std::memset(img, 0, ly.total);
+  constexpr int NC = L + 1, NG = n_groups(L);
+  double* sw = reinterpret_cast<double*>(img + ly.sw);
+  for (int i = 0; i < kMaxN + 2 + NC; ++i) sw[i] = i < kMaxN + 2 ? a.w[i] : 0.0;
+  if (ly.need_w) {
+    double* w1 = reinterpret_cast<double*>(img + ly.sW1);
+    double* w2 = reinterpret_cast<double*>(img + ly.sW2);
+    for (int i = 0; i < kMaxN + 2; ++i) {
+      double s1 = 0.0, s2 = 0.0;
+      for (int c = 0; c < NC; ++c) {
+        s1 = std::fma(sw[i + c], a.b_cls[c], s1);
+        s2 = std::fma(sw[i + c] * a.b_cls[c], a.e_cls[c], s2);
+      }
+      w1[i] = s1;
+      w2[i] = s2;
+    }
+  }
+  auto gray_groups = [&](int slot, double2* dst, bool small_only) {
+    int k = 0;
+    for (int c = 0; c <= L; ++c) {
+      if (small_only && i15_class(L, c)) continue;
+      for (int g = 0; g < class_groups(L, c); ++g, ++k)
+        for (int sl = 0; sl < kGraySlots; ++sl)
+          dst[k * kGraySlots + sl] = gray_table_entry(&a.gpre[slot][group_base(L, c) + g][0], (unsigned)sl, true);
+    }
+    (void)NG;
+  };
+  if (ly.nt > 0) gray_groups(0, reinterpret_cast<double2*>(img + ly.sgray0), ly.i15);
+  if (ly.nt > 1) gray_groups(1, reinterpret_cast<double2*>(img + ly.sgray1), false);
+  if (ly.i15) {
+    double2* et = reinterpret_cast<double2*>(img + ly.si15);
+    for (int c = 0; c <= L; ++c) {
+      if (!i15_class(L, c)) continue;
+      const int len = binom(L, c), i0 = class_start(L, c), base = i15_base(L, c), slots = i15_slots(L, c);
+      for (int t = 0; t < 2 * slots; ++t) {
+        unsigned n = (unsigned)(t >> 1);
+        for (int sh = 1; sh < 16; sh <<= 1) n ^= n >> sh;  // Gray -> binary
+        double2 v = make_double2(0.0, 0.0);
+        auto packed = [](unsigned hi, float lo) {
+          unsigned long long b = ((unsigned long long)hi << 32);
+          unsigned lb;
+          std::memcpy(&lb, &lo, sizeof lb);
+          b |= lb;
+          double d;
+          std::memcpy(&d, &b, sizeof d);
+          return d;
+        };
+        if ((int)n < len) {
+          if ((t & 1) == 0)
+            v = make_double2(a.cpre[0][i0 + c + n], packed(a.xq[0][i0 + n] & 0xFFFFu, (float)n));
+          else
+            v = make_double2(a.cpre[0][i0 + c + a.te[0][i0 + n]], a.tab[i0 + n]);
+        } else if ((int)n == len) {
+          v = (t & 1) == 0 ? make_double2(a.cpre[0][i0 + c + len], packed(0xFFFFu, (float)len))
+                           : make_double2(a.cpre[0][i0 + c + len], 0.0);
+        }
+        et[2 * base + t] = v;
+      }
+    }
+    std::memcpy(img + ly.sxq, a.xq[0], sizeof(unsigned) << L);
+    std::memcpy(img + ly.ste, a.te[0], (size_t)1 << L);
+  }
+}
+
 template <int L>
 static int fill_fast_args(const bp_tree* t, const Layout& lay, unsigned km, std::vector<unsigned char>& buf) {
   buf.assign(sizeof(ExactArgs<L>), 0);
@@ -373,6 +444,10 @@ static int fill_fast_args(const bp_tree* t, const Layout& lay, unsigned km, std:
   s.n_mid = 1 << m;
   s.q = lay.q;
   s.zero = 0;
+  // the shared-memory image after the block (K1's CTA setup copies it)
+  const size_t head = align16(sizeof(ExactArgs<L>));
+  buf.resize(head + k1_smem_layout<L>(km).total, 0);
+  build_smem_image<L>(*reinterpret_cast<ExactArgs<L>*>(buf.data()), km, buf.data() + head);
   return BP_OK;
 }
 
@@ -485,11 +560,13 @@ static void set_contract(std::vector<unsigned char>& buf, int L, const bp_tree* 
   s->NK = (double)t->n_steps * t->K;
 }
 
-static int build_fast_args(const bp_tree* t, const Layout& lay, unsigned km, std::vector<unsigned char>& buf) {
+static int build_fast_args(const bp_tree* t, const Layout& lay, unsigned km, std::vector<unsigned char>& buf,
+                           FastArgsKey* key_out = nullptr) {
   static std::mutex mu;
   static std::list<std::pair<FastArgsKey, std::vector<unsigned char>>> lru;  // most recent first
   constexpr size_t kCap = 16;
   const FastArgsKey key{lay.L, lay.D, lay.m, lay.Dp, lay.q, t->n_steps, km, t->u, t->d, t->up_probs[0], t->disc};
+  if (key_out) *key_out = key;
   {
     std::lock_guard<std::mutex> g(mu);
     for (auto it = lru.begin(); it != lru.end(); ++it)
@@ -511,6 +588,35 @@ static int build_fast_args(const bp_tree* t, const Layout& lay, unsigned km, std
   lru.emplace_front(key, buf);
   if (lru.size() > kCap) lru.pop_back();
   return BP_OK;
+}
+
+// Device images of K1 argument blocks (the tables K1's CTA setup reads;
+// k_exact_fast's `ga`), per device, keyed by lattice + layout + kinds.  Kept
+// for the life of the process (graphs captured with them stay valid), at most
+// kMaxImages per device; beyond that a plan uploads (and frees) its own.
+struct DevArgImage {
+  FastArgsKey key;
+  void* p;
+};
+static std::mutex g_img_mu;
+static std::vector<DevArgImage> g_img[64];
+constexpr size_t kMaxImages = 256;
+
+// the device's cached image for key (uploaded on first use), or nullptr when
+// the cache is full.  Not callable inside a stream capture.
+static void* cached_arg_image(int dev, const FastArgsKey& key, const std::vector<unsigned char>& args) {
+  std::lock_guard<std::mutex> g(g_img_mu);
+  for (auto& im : g_img[dev])
+    if (im.key == key) return im.p;
+  if (g_img[dev].size() >= kMaxImages) return nullptr;
+  void* p = nullptr;
+  if (cudaMalloc(&p, args.size()) != cudaSuccess) return nullptr;
+  if (cudaMemcpy(p, args.data(), args.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+    cudaFree(p);
+    return nullptr;
+  }
+  g_img[dev].push_back(DevArgImage{key, p});
+  return p;
 }
 
 static void set_units_w(std::vector<unsigned char>& buf, unsigned long long u0, unsigned long long u1) {
@@ -605,6 +711,9 @@ struct bp_exact_plan {
   struct Group {
     unsigned km;
     std::vector<unsigned char> args;
+    FastArgsKey key{};           // class engine: the lattice key of args
+    void* dargs[64] = {nullptr};  // class engine: device image per device
+    bool dargs_owned[64] = {false};
   };
   std::vector<Group> groups;
   GenericArgs gen{};
@@ -659,7 +768,7 @@ static int plan_build(const bp_tree* t, uint32_t payoffs, uint32_t flags, bp_exa
     for (unsigned km : fast_groups(payoffs)) {
       bp_exact_plan::Group g;
       g.km = km;
-      int rc = build_fast_args(&P->tree, lay, km, g.args);
+      int rc = build_fast_args(&P->tree, lay, km, g.args, &g.key);
       if (rc) return rc;
       P->groups.push_back(std::move(g));
     }
@@ -748,9 +857,15 @@ static int plan_build(const bp_tree* t, uint32_t payoffs, uint32_t flags, bp_exa
 // device `dev` (current).  out_dev: [sb_count][6][2] doubles (device).
 // The plan's scratch for `dev` is reused: calls on one plan and device must
 // be issued on one stream (stream order protects the reuse).
+static int plan_attach_images(bp_exact_plan* P, int dev, cudaStream_t st);
+
 static int plan_enqueue(bp_exact_plan* P, int dev, int sb_first, int sb_count, double* out_dev,
                         unsigned long long* hist_dev, cudaStream_t st) {
   const Layout& lay = P->lay;
+  if (dev >= 0 && dev < 64) {
+    const int rc = plan_attach_images(P, dev, st);  // a no-op once attached (always so inside captures)
+    if (rc) return rc;
+  }
   if (sb_first < 0 || sb_count < 1 || sb_first + sb_count > lay.n_sb)
     return fail(BP_E_RANK_RANGE, "super-block range [" + std::to_string(sb_first) + ", " +
                                      std::to_string(sb_first + sb_count) + ") outside [0, " +
@@ -820,11 +935,16 @@ static int plan_enqueue(bp_exact_plan* P, int dev, int sb_first, int sb_count, d
     for (auto& g : P->groups) {
       const bool cnt_g = cnt && first_group;
       first_group = false;
-      set_units(g.args, lay.L, u0, u1);
+      // diagnostics: BINPATHS_K1_EMPTY=1 launches K1 with no units (its fixed cost: table setup)
+      static const bool k1_empty = [] {
+        const char* e = std::getenv("BINPATHS_K1_EMPTY");
+        return e && std::atoi(e) != 0;
+      }();
+      set_units(g.args, lay.L, u0, k1_empty ? u0 : u1);
       const int occ = std::max(1, cached_occupancy_fast(lay.L, g.km, cnt_g));
       const int grid = (int)std::max<unsigned long long>(1, std::min<unsigned long long>(want, (unsigned long long)occ * sms));
       const auto tl0 = std::chrono::steady_clock::now();
-      BP_CUDA(launch_exact_fast(lay.L, g.km, g.args.data(), cnt_g, grid, st, unit_base, hist_dev));
+      BP_CUDA(launch_exact_fast(lay.L, g.km, g.args.data(), cnt_g, grid, st, unit_base, hist_dev, g.dargs[dev]));
       const auto tl1 = std::chrono::steady_clock::now();
       if (trace_on())
         std::fprintf(stderr, "[bp trace] K1 launch %.1f us (%zu B of arguments)\n",
@@ -842,6 +962,46 @@ static int plan_enqueue(bp_exact_plan* P, int dev, int sb_first, int sb_count, d
     BP_CUDA(launch_sb_reduce(unit_base, lay.units_per_sb, sb_first, sb_count, P->payoffs, std::exchange(zero_kinds, 0u), 1.0, out_dev, st));
   }
   return BP_OK;
+}
+
+// Attach every class-engine group's device argument image on dev: the
+// process cache, else an image the plan owns (stream-ordered allocation on
+// st).  Outside any stream capture.
+static int plan_attach_images(bp_exact_plan* P, int dev, cudaStream_t st) {
+  if (P->lay.engine != 1) return BP_OK;
+  for (auto& g : P->groups) {
+    if (g.dargs[dev]) continue;
+    void* p = cached_arg_image(dev, g.key, g.args);
+    if (!p) {
+      BP_CUDA(cudaMallocAsync(&p, g.args.size(), st));
+      BP_CUDA(cudaMemcpyAsync(p, g.args.data(), g.args.size(), cudaMemcpyHostToDevice, st));
+      g.dargs_owned[dev] = true;
+    }
+    g.dargs[dev] = p;
+  }
+  return BP_OK;
+}
+
+static bool plan_images_cached(const bp_exact_plan* P, int dev) {
+  for (auto& g : P->groups)
+    if (!g.dargs[dev] || g.dargs_owned[dev]) return false;
+  return true;
+}
+
+// free the plan's own images, stream-ordered on st for device `dev_st` (the
+// current device), after a device sync for the others
+static void plan_release_images(bp_exact_plan* P, cudaStream_t st) {
+  int cur = 0;
+  cudaGetDevice(&cur);
+  for (auto& g : P->groups)
+    for (int d = 0; d < 64; ++d)
+      if (g.dargs_owned[d] && g.dargs[d]) {
+        cudaSetDevice(d);
+        cudaFreeAsync(g.dargs[d], d == cur ? st : 0);
+        g.dargs[d] = nullptr;
+        g.dargs_owned[d] = false;
+      }
+  cudaSetDevice(cur);
 }
 
 static void plan_release_scratch(bp_exact_plan* P, cudaStream_t st) {
@@ -874,6 +1034,7 @@ static int enqueue_superblocks(const bp_tree* t, uint32_t payoffs, uint32_t flag
   int rc = plan_build(t, payoffs, flags, &P);
   if (rc) return rc;
   rc = plan_enqueue(&P, dev, sb_first, sb_count, out_dev, hist_dev, st);
+  plan_release_images(&P, st);  // stream-ordered: after the kernels
   if (P.scratch[dev].p) cudaFreeAsync(P.scratch[dev].p, st);  // stream-ordered: after the kernels
   P.scratch[dev].p = nullptr;
   if (P.th_dev[dev]) {  // K8 tables: the synchronous path frees them after the stream drains
@@ -935,6 +1096,7 @@ static bool plan_enqueue_graph(bp_exact_plan* P, int dev, int sb_first, int sb_c
     }
   }
   for (auto& g : P->groups) cached_occupancy_fast(P->lay.L, g.km, false);  // no queries inside the capture
+  if (plan_attach_images(P, dev, st) != BP_OK) return false;  // uploads happen outside the capture
   cudaStream_t cap;
   if (cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking) != cudaSuccess) return false;
   cudaGraph_t graph = nullptr;
@@ -980,6 +1142,7 @@ extern "C" void bp_exact_plan_destroy(bp_exact_plan* plan) {
   if (!plan) return;
   for (auto& g : plan->graphs) cudaGraphExecDestroy(g.exec);
   plan_release_scratch(plan, 0);
+  plan_release_images(plan, 0);
   delete plan;
 }
 
@@ -1131,6 +1294,8 @@ static bool try_graph_job(DevCtx& c, bp_exact_plan& P, DeviceJob* job, uint32_t 
     c.scratch_bytes = need;
   }
   for (auto& g : P.groups) cached_occupancy_fast(P.lay.L, g.km, false);  // no queries inside the capture
+  // argument images from the process cache (they outlive this call's plan)
+  if (plan_attach_images(&P, dev, c.st) != BP_OK || !plan_images_cached(&P, dev)) return false;
   std::vector<unsigned char> key;
   graph_key(key, P.lay, &P.tree, P.payoffs, flags, job, c.scratch);
   const size_t np = (size_t)job->sb_count * BP_N_PAYOFFS * 2;
@@ -1245,6 +1410,7 @@ static void run_device_job(const bp_tree* t, uint32_t payoffs, uint32_t flags, D
     job->err = g_err;
     cudaStreamSynchronize(c.st);
     plan_release_scratch(&P, c.st);
+    plan_release_images(&P, c.st);
     return;
   }
   cudaEventRecord(c.e1, c.st);
@@ -1264,6 +1430,7 @@ static void run_device_job(const bp_tree* t, uint32_t payoffs, uint32_t flags, D
   if (cnt) std::memcpy(job->hist.data(), c.hist_host, sizeof(unsigned long long) * 66);
   cudaEventElapsedTime(&job->ms, c.e0, c.e1);
   plan_release_scratch(&P, c.st);
+  plan_release_images(&P, c.st);
 }
 
 extern "C" int bp_exact(const bp_tree* tree, uint32_t payoffs, uint32_t flags, int n_dev, const int* devices,

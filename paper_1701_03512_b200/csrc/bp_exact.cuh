@@ -167,6 +167,52 @@ __host__ __device__ inline unsigned i15_map(float vf, float s, float o) {
 #endif
 }
 
+// K1's shared-memory tables as one contiguous image (byte offsets), a
+// function of (L, kind mask): the host builds the image once per lattice
+// (bp_capi.cu build_smem_image) after the argument block, and every CTA
+// copies it with coalesced 16-byte loads instead of computing the tables.
+__host__ __device__ constexpr size_t align16(size_t v) { return (v + 15) & ~(size_t)15; }
+struct K1SmemLayout {
+  bool i15, need_w;
+  int nt, ng0, ng1;
+  size_t sw, sW1, sW2, sgray0, sgray1, si15, sxq, ste, total;
+};
+__host__ __device__ constexpr int kind_tables(unsigned km) {
+  return (int)((km >> kAC) & 1) + (int)((km >> kAP) & 1) + (int)((km >> kFL) & 1) + (int)((km >> kFLP) & 1);
+}
+template <int L>
+__host__ __device__ constexpr K1SmemLayout k1_smem_layout(unsigned km) {
+  K1SmemLayout o{};
+  o.nt = kind_tables(km);
+  o.i15 = i15_on<L>() && (((km >> kAC) & 1) || ((km >> kAP) & 1));
+  o.need_w = ((km >> kFL) & 1) || ((km >> kFLP) & 1);
+  o.ng1 = n_groups(L);
+  int small = 0;
+  for (int c = 0; c <= L; ++c)
+    if (!i15_class(L, c)) small += class_groups(L, c);
+  o.ng0 = o.i15 ? small : n_groups(L);
+  constexpr int kSlots = 64;  // Gray-table slots per group (kGraySlots, bp_leaf.cuh)
+  size_t off = 0;
+  o.sw = off;
+  off = align16(off + sizeof(double) * (kMaxN + 2 + L + 1));
+  o.sW1 = off;
+  off += o.need_w ? sizeof(double) * (kMaxN + 2) : 0;
+  o.sW2 = off;
+  off = align16(off + (o.need_w ? sizeof(double) * (kMaxN + 2) : 0));
+  o.sgray0 = off;
+  off += o.nt > 0 ? (size_t)16 * o.ng0 * kSlots : 0;
+  o.sgray1 = off;
+  off += o.nt > 1 ? (size_t)16 * o.ng1 * kSlots : 0;
+  o.si15 = off;
+  off += o.i15 ? (size_t)32 * i15_entries(L) : 0;
+  o.sxq = off;
+  off += o.i15 ? (size_t)4 << L : 0;
+  o.ste = off;
+  off += o.i15 ? (size_t)1 << L : 0;
+  o.total = align16(off);
+  return o;
+}
+
 template <int L>
 struct __align__(16) ExactArgs {
   // inner tables by position (class-major, sorted in the compare direction

@@ -49,7 +49,9 @@ __global__ void __launch_bounds__(256, fast_tables(KM) == 2                     
                                        : (i15_on<L>() && (KM & ((1u << kAC) | (1u << kAP))))     ? BP_MINB_I15
                                                                                                  : BP_MINB1)
 k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_out,
-             unsigned long long* __restrict__ hist) {
+             unsigned long long* __restrict__ hist, const ExactArgs<L>* __restrict__ ga) {
+  // ga: the device copy of the argument block followed by the shared-memory
+  // image (below); the leaf loops read the parameter bank (uniform loads).
   constexpr int NC = L + 1;
   constexpr int NG = n_groups(L);
   constexpr bool kAC_ = (KM >> kAC) & 1, kAP_ = (KM >> kAP) & 1, kFL_ = (KM >> kFL) & 1,
@@ -63,35 +65,92 @@ k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_
   // nodes per leaf block: each table load feeds NP compares
   constexpr int NP = kNodesPerBlock;
 
-  __shared__ double sw[kMaxN + 2 + NC];
   __shared__ unsigned long long shist[kMaxN + 2];
-#if BP_GRAY
-  // I15 screen on the Asian slot (slot 0; the lookback thresholds are ratios
+#if BP_GRAY && BP_FOLD && !BP_TAB_SMEM
+  // The shared tables as ONE image (k1_smem_layout): the weights (zero
+  // padded), the lookback kinds' W1/W2, the Gray tables (I15: only the small
+  // classes' on the Asian slot 0), and the I15 entry tables, screened values
+  // and tie-run ends of slot 0.  The host builds the image once per lattice
+  // after the argument block (ga); every CTA copies it with 16-byte loads.
+  // The I15 screen runs on the Asian slot; the lookback thresholds are ratios
   // of lattice prices that tie with the table values, so those kinds keep the
-  // fp64 block): its entry tables, screened values and tie-run ends, and the
-  // Gray tables of the classes it leaves to the fp64 block; the other slot
-  // keeps all its Gray tables
-#ifndef BP_I15_LOOKBACK
-#define BP_I15_LOOKBACK 0  // diagnostics: 1 = the screen on the lookback slot too (r2 scan: no gain)
-#endif
-  constexpr bool I15 = i15_on<L>() && (kAC_ || kAP_ || (BP_I15_LOOKBACK && NT == 1));
-  constexpr int NG0 = I15 ? n_small_groups<L>() : NG;
-  __shared__ __align__(16) double2 sgray0[NT > 0 ? NG0 * kGraySlots : 1];
-  __shared__ __align__(16) double2 sgray1[NT > 1 ? NG * kGraySlots : 1];
-  __shared__ __align__(16) double2 si15[I15 ? 2 * i15_entries(L) : 1];
-  __shared__ __align__(16) unsigned sxq[I15 ? (1 << L) : 4];
-  __shared__ unsigned char ste[I15 ? (1 << L) : 4];
-  if constexpr (I15) {
-    gray_fill_small<L, 0>(a.gpre[0], sgray0);
-    i15_fill<L, 0>(ParamTabs<L, 0>{a}, si15);
-    for (int i = threadIdx.x; i < (1 << L); i += blockDim.x) {
-      sxq[i] = a.xq[0][i];
-      ste[i] = a.te[0][i];
+  // fp64 block.
+  constexpr K1SmemLayout LY = k1_smem_layout<L>(KM);
+  constexpr bool I15 = LY.i15;
+  constexpr bool needW = LY.need_w;
+  static_assert(kGraySlots == 64, "k1_smem_layout assumes 64 Gray slots per group");
+  __shared__ __align__(16) unsigned char simg[LY.total];
+  double* sw = reinterpret_cast<double*>(simg + LY.sw);
+  double* sW1 = reinterpret_cast<double*>(simg + LY.sW1);
+  double* sW2 = reinterpret_cast<double*>(simg + LY.sW2);
+  const double2* sgray0 = reinterpret_cast<const double2*>(simg + LY.sgray0);
+  const double2* sgray1 = reinterpret_cast<const double2*>(simg + LY.sgray1);
+  const double2* si15 = reinterpret_cast<const double2*>(simg + LY.si15);
+  const unsigned* sxq = reinterpret_cast<const unsigned*>(simg + LY.sxq);
+  const unsigned char* ste = simg + LY.ste;
+  if (ga) {
+    const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(ga) + align16(sizeof(ExactArgs<L>)));
+    uint4* dst = reinterpret_cast<uint4*>(simg);
+    // every load of the thread issued before the first store (one memory latency)
+    constexpr int n16 = (int)(LY.total / 16), per = (n16 + 255) / 256;
+    uint4 v[per];
+#pragma unroll
+    for (int r = 0; r < per; ++r) {
+      const int i = threadIdx.x + 256 * r;
+      if (i < n16) v[r] = __ldg(src + i);
     }
-  } else if constexpr (NT > 0) {
+#pragma unroll
+    for (int r = 0; r < per; ++r) {
+      const int i = threadIdx.x + 256 * r;
+      if (i < n16) dst[i] = v[r];
+    }
+  } else {
+    // no image: build the tables here from the parameter bank
+    double* w_ = reinterpret_cast<double*>(simg + LY.sw);
+    for (int i = threadIdx.x; i < kMaxN + 2 + NC; i += blockDim.x) w_[i] = (i < kMaxN + 2) ? a.w[i] : 0.0;
+    double2* g0 = reinterpret_cast<double2*>(simg + LY.sgray0);
+    double2* g1 = reinterpret_cast<double2*>(simg + LY.sgray1);
+    if constexpr (I15) {
+      gray_fill_small<L, 0>(a.gpre[0], g0);
+      i15_fill<L, 0>(ParamTabs<L, 0>{a}, reinterpret_cast<double2*>(simg + LY.si15));
+      for (int i = threadIdx.x; i < (1 << L); i += blockDim.x) {
+        reinterpret_cast<unsigned*>(simg + LY.sxq)[i] = a.xq[0][i];
+        simg[LY.ste + i] = a.te[0][i];
+      }
+    } else if constexpr (NT > 0) {
+      for (int i = threadIdx.x; i < NG * kGraySlots; i += blockDim.x)
+        g0[i] = gray_table_entry(&a.gpre[0][i / kGraySlots][0], (unsigned)(i % kGraySlots), true);
+    }
+    if constexpr (NT > 1)
+      for (int i = threadIdx.x; i < NG * kGraySlots; i += blockDim.x)
+        g1[i] = gray_table_entry(&a.gpre[1][i / kGraySlots][0], (unsigned)(i % kGraySlots), true);
+    if constexpr (needW) {
+      __syncthreads();
+      // W1[h] = sum_c w[h+c] C(L,c), W2[h] = sum_c w[h+c] C(L,c) e_c (the lookback
+      // kinds' out-of-the-money and terminal terms), fixed order
+      for (int i = threadIdx.x; i < kMaxN + 2; i += blockDim.x) {
+        double w1 = 0.0, w2 = 0.0;
+        for (int c = 0; c < NC; ++c) {
+          w1 = fma(w_[i + c], a.b_cls[c], w1);
+          w2 = fma(w_[i + c] * a.b_cls[c], a.e_cls[c], w2);
+        }
+        sW1[i] = w1;
+        sW2[i] = w2;
+      }
+    }
+  }
+#define BP_GTAB(SLOT) reinterpret_cast<const char*>((SLOT) == 0 ? &sgray0[0] : &sgray1[0])
+#define BP_LEAF(SLOT, GTV, TH) leaf_block_gray<L, NP, SLOT, GTV>(tb, BP_GTAB(SLOT), TH, acc, cnt)
+#else
+  // diagnostic configurations (BP_GRAY=0, BP_FOLD=0, BP_TAB_SMEM=1): tables built here
+  constexpr bool I15 = false;
+  __shared__ double sw[kMaxN + 2 + NC];
+#if BP_GRAY
+  __shared__ __align__(16) double2 sgray0[NT > 0 ? NG * kGraySlots : 1];
+  __shared__ __align__(16) double2 sgray1[NT > 1 ? NG * kGraySlots : 1];
+  if constexpr (NT > 0)
     for (int i = threadIdx.x; i < NG * kGraySlots; i += blockDim.x)
       sgray0[i] = gray_table_entry(&a.gpre[0][i / kGraySlots][0], (unsigned)(i % kGraySlots), BP_FOLD != 0);
-  }
   if constexpr (NT > 1)
     for (int i = threadIdx.x; i < NG * kGraySlots; i += blockDim.x)
       sgray1[i] = gray_table_entry(&a.gpre[1][i / kGraySlots][0], (unsigned)(i % kGraySlots), BP_FOLD != 0);
@@ -109,8 +168,6 @@ k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_
 #endif
   for (int i = threadIdx.x; i < kMaxN + 2 + NC; i += blockDim.x) sw[i] = (i < kMaxN + 2) ? a.w[i] : 0.0;
 #if BP_FOLD
-  // per node up count h: W1[h] = sum_c w[h+c] C(L,c), W2[h] = sum_c w[h+c] C(L,c) e_c (the lookback
-  // kinds' out-of-the-money and terminal terms), fixed order
   constexpr bool needW = kFL_ || kFLP_;
   __shared__ double sW1[needW ? kMaxN + 2 : 1], sW2[needW ? kMaxN + 2 : 1];
   if (needW) {
@@ -125,6 +182,7 @@ k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_
       sW2[i] = w2;
     }
   }
+#endif
 #endif
   if (CNT)
     for (int i = threadIdx.x; i < kMaxN + 2; i += blockDim.x) shist[i] = 0ull;
@@ -348,12 +406,13 @@ k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_
 // launch wrappers
 template <int L, unsigned KM>
 cudaError_t launch_fast_t(const void* args, bool cnt, int grid, cudaStream_t st, double2* unit_out,
-                                 unsigned long long* hist) {
+                          unsigned long long* hist, const void* dev_args) {
   const ExactArgs<L>& a = *static_cast<const ExactArgs<L>*>(args);
+  const ExactArgs<L>* ga = static_cast<const ExactArgs<L>*>(dev_args);
   if (cnt)
-    k_exact_fast<L, KM, true><<<grid, 256, 0, st>>>(a, unit_out, hist);
+    k_exact_fast<L, KM, true><<<grid, 256, 0, st>>>(a, unit_out, hist, ga);
   else
-    k_exact_fast<L, KM, false><<<grid, 256, 0, st>>>(a, unit_out, hist);
+    k_exact_fast<L, KM, false><<<grid, 256, 0, st>>>(a, unit_out, hist, ga);
   return cudaGetLastError();
 }
 

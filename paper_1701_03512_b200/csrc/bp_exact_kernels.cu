@@ -77,45 +77,48 @@ k_exact_generic(const __grid_constant__ GenericArgs a, double2* __restrict__ uni
 
 // ---------------------------------------------------------------------------
 // K2: super-block reduce.  Block b reduces the units of super-block
-// sb_first + b in a fixed order (thread-contiguous chunks, fixed tree), and
-// writes (sum, comp) per kind scaled by scale[k] (1/N for Asian kinds).
-// Kinds in zero_kinds (requested by no launch group of the valuation) are
-// written as 0, so every output entry is written exactly once per step.
+// sb_first + b in a fixed order -- thread t merges units t, t + 256, ... in
+// ascending order, then a fixed warp shuffle tree (warp_comp_reduce), then
+// warp 0 merges the 8 warp sums the same way -- and writes (sum, comp) per
+// kind scaled by scale[k] (1/N for Asian kinds).  Kinds in zero_kinds
+// (requested by no launch group of the valuation) are written as 0, so every
+// output entry is written exactly once per step.
 __global__ void __launch_bounds__(256)
 k_sb_reduce(const double2* __restrict__ unit_out, unsigned long long units_per_sb, int sb_first,
             unsigned kinds, unsigned zero_kinds, double scale_asian, double* __restrict__ out) {
-  __shared__ double ss[256], sc2[256];
+  __shared__ double ws[kNumKinds][8], wc[kNumKinds][8];
   const unsigned long long u0 = (unsigned long long)(sb_first + blockIdx.x) * units_per_sb;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x < 2 * kNumKinds && ((zero_kinds >> (threadIdx.x >> 1)) & 1))
     out[blockIdx.x * kNumKinds * 2 + threadIdx.x] = 0.0;
+  // all of the thread's loads first (every kind), then the merges
+#pragma unroll
   for (int k = 0; k < kNumKinds; ++k) {
     if (!((kinds >> k) & 1)) continue;
     double s = 0.0, c = 0.0;
-    const unsigned long long per = (units_per_sb + blockDim.x - 1) / blockDim.x;
-    const unsigned long long lo = threadIdx.x * per;
-    const unsigned long long hi = lo + per < units_per_sb ? lo + per : units_per_sb;
-    for (unsigned long long u = lo; u < hi; ++u) {
+    for (unsigned long long u = threadIdx.x; u < units_per_sb; u += blockDim.x) {
       const double2 v = unit_out[(u0 + u) * kNumKinds + k];
       comp_merge(s, c, v.x, v.y);
     }
-    ss[threadIdx.x] = s;
-    sc2[threadIdx.x] = c;
-    __syncthreads();
-    for (int stride = blockDim.x / 2; stride > 0; stride >>= 1) {
-      if (threadIdx.x < stride) {
-        double a_s = ss[threadIdx.x], a_c = sc2[threadIdx.x];
-        comp_merge(a_s, a_c, ss[threadIdx.x + stride], sc2[threadIdx.x + stride]);
-        ss[threadIdx.x] = a_s;
-        sc2[threadIdx.x] = a_c;
+    warp_comp_reduce(s, c);
+    if (lane == 0) {
+      ws[k][warp] = s;
+      wc[k][warp] = c;
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int k = 0; k < kNumKinds; ++k) {
+      if (!((kinds >> k) & 1)) continue;
+      double s = lane < 8 ? ws[k][lane] : 0.0, c = lane < 8 ? wc[k][lane] : 0.0;
+      warp_comp_reduce(s, c);
+      if (lane == 0) {
+        const double f = (k == kAC || k == kAP) ? scale_asian : 1.0;
+        out[(blockIdx.x * kNumKinds + k) * 2 + 0] = s * f;
+        out[(blockIdx.x * kNumKinds + k) * 2 + 1] = c * f;
       }
-      __syncthreads();
     }
-    if (threadIdx.x == 0) {
-      const double f = (k == kAC || k == kAP) ? scale_asian : 1.0;
-      out[(blockIdx.x * kNumKinds + k) * 2 + 0] = ss[0] * f;
-      out[(blockIdx.x * kNumKinds + k) * 2 + 1] = sc2[0] * f;
-    }
-    __syncthreads();
   }
 }
 
@@ -124,7 +127,7 @@ k_sb_reduce(const double2* __restrict__ unit_out, unsigned long long units_per_s
 // (L, kind mask) in bp_exact_fast_inst.cu (compiled once per BP_FAST_PART).
 template <int L, unsigned KM>
 cudaError_t launch_fast_t(const void* args, bool cnt, int grid, cudaStream_t st, double2* unit_out,
-                          unsigned long long* hist);
+                          unsigned long long* hist, const void* dev_args);
 template <int L, unsigned KM>
 int occupancy_fast_t(bool cnt);
 
@@ -141,9 +144,9 @@ bool fast_kind_mask_supported(unsigned km) {
 }
 
 cudaError_t launch_exact_fast(int L, unsigned km, const void* args, bool cnt, int grid, cudaStream_t st,
-                              double2* unit_out, unsigned long long* hist) {
+                              double2* unit_out, unsigned long long* hist, const void* dev_args) {
 #define BP_CASE(LL, KMV) \
-  if (L == LL && km == (KMV)) return launch_fast_t<LL, (KMV)>(args, cnt, grid, st, unit_out, hist);
+  if (L == LL && km == (KMV)) return launch_fast_t<LL, (KMV)>(args, cnt, grid, st, unit_out, hist, dev_args);
   BP_FAST_KMS(BP_CASE, 8)
   BP_FAST_KMS(BP_CASE, 9)
 #undef BP_CASE

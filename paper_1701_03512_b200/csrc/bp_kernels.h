@@ -9,8 +9,9 @@
 namespace bp {
 
 bool fast_kind_mask_supported(unsigned km);
+// dev_args: a device copy of the argument block's tables (CTA setup reads), or nullptr
 cudaError_t launch_exact_fast(int L, unsigned km, const void* args, bool cnt, int grid, cudaStream_t st,
-                              double2* unit_out, unsigned long long* hist);
+                              double2* unit_out, unsigned long long* hist, const void* dev_args);
 int occupancy_exact_fast(int L, unsigned km, bool cnt);
 size_t exact_args_size(int L);
 

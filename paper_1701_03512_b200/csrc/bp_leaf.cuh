@@ -96,11 +96,16 @@ constexpr int kGraySlots = gray_slots(kGroup);
 
 // entry of Gray code g of a group from its prefix sums pre[0..kGroup]:
 // {P[n], n} with n as the low word of .y (int counts) or as a double (fold)
-__device__ inline double2 gray_table_entry(const double* pre, unsigned g, bool count_as_double) {
+__host__ __device__ inline double2 gray_table_entry(const double* pre, unsigned g, bool count_as_double) {
   unsigned n = g;
   for (int s = 1; s < 16; s <<= 1) n ^= n >> s;  // Gray -> binary
   if (n > (unsigned)kGroup) return make_double2(0.0, 0.0);
-  return make_double2(pre[n], count_as_double ? (double)n : __longlong_as_double((long long)n));
+  double y = (double)n;
+  if (!count_as_double) {
+    const long long v = (long long)n;
+    std::memcpy(&y, &v, sizeof y);
+  }
+  return make_double2(pre[n], y);
 }
 
 template <int L, int NP, int SLOT, bool GT, int C, int G>
