@@ -42,7 +42,7 @@ __host__ __device__ constexpr int fast_tables(unsigned km) {
 #define BP_MINB2 2  // ... and by the fused two-table kernels
 #endif
 #ifndef BP_MINB_I15
-#define BP_MINB_I15 3  // ... and by the one-table kernels of the Asian kinds (I15 screen)
+#define BP_MINB_I15 2  // ... and by the one-table kernels of the Asian kinds (I15 screen; r2 scan: 2 beats 3 by 6 % at N=36)
 #endif
 template <int L, unsigned KM, bool CNT>
 __global__ void __launch_bounds__(256, fast_tables(KM) == 2                                      ? BP_MINB2
