@@ -193,7 +193,7 @@ k_exact_batch(const BatchOption* __restrict__ opts, BatchArgs ba, double2* __res
       }
     }
     __syncthreads();
-    i15_fill<kBL, 0>(SmemTabs{i15_s, i15_o, tab, i15_cpre, i15_xq, i15_te}, i15_et);
+    i15_fill<kBL, 0>(SmemTabs{i15_s, i15_o, tab, i15_cpre, i15_xq, i15_te}, i15_et, false);
   } else if (TAB) {
     for (int i = tid; i < NG * kGraySlots; i += kBThreads)
       sgray[i] = gray_table_entry(&gpre[(i / kGraySlots) * kGroupSlots], (unsigned)(i % kGraySlots), true);

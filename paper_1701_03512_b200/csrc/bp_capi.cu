@@ -308,6 +308,17 @@ static void i15_layout(int kind, const double* pos, ExactArgs<L>& a, int slot) {
   }
 }
 
+// the screen tables of one slot of a host argument block (i15_quarter)
+template <int L>
+struct HostTabs {
+  const ExactArgs<L>& a;
+  int slot;
+  __host__ __device__ double tab(int i) const { return a.tab[slot * (1 << L) + i]; }
+  __host__ __device__ double cpre(int i) const { return a.cpre[slot][i]; }
+  __host__ __device__ unsigned xq(int i) const { return a.xq[slot][i]; }
+  __host__ __device__ unsigned te(int i) const { return a.te[slot][i]; }
+};
+
 // K1's shared-memory image (k1_smem_layout), appended to the argument block:
 // the tables every CTA used to build from the parameter bank, built once here
 // with the same formulas (kernel fallback: bp_exact_fast.cuh, ga == nullptr).
@@ -341,40 +352,23 @@ static void build_smem_image(const ExactArgs<L>& a, unsigned km, unsigned char* 
     }
     (void)NG;
   };
-  if (ly.nt > 0) gray_groups(0, reinterpret_cast<double2*>(img + ly.sgray0), ly.i15);
-  if (ly.nt > 1) gray_groups(1, reinterpret_cast<double2*>(img + ly.sgray1), false);
-  if (ly.i15) {
-    double2* et = reinterpret_cast<double2*>(img + ly.si15);
+  for (int slot = 0; slot < ly.nt && slot < 2; ++slot) {
+    gray_groups(slot, reinterpret_cast<double2*>(img + ly.sgray[slot]), ly.i15[slot]);
+    if (!ly.i15[slot]) continue;
+    double2* et = reinterpret_cast<double2*>(img + ly.si15[slot]);
+    const HostTabs<L> ht{a, slot};
     for (int c = 0; c <= L; ++c) {
       if (!i15_class(L, c)) continue;
       const int len = binom(L, c), i0 = class_start(L, c), base = i15_base(L, c), slots = i15_slots(L, c);
-      for (int t = 0; t < 2 * slots; ++t) {
-        unsigned n = (unsigned)(t >> 1);
+      const int nq = i15_entry_bytes(ly.lookback[slot]) / 16;
+      for (int t = 0; t < nq * slots; ++t) {
+        unsigned n = (unsigned)(t / nq);
         for (int sh = 1; sh < 16; sh <<= 1) n ^= n >> sh;  // Gray -> binary
-        double2 v = make_double2(0.0, 0.0);
-        auto packed = [](unsigned hi, float lo) {
-          unsigned long long b = ((unsigned long long)hi << 32);
-          unsigned lb;
-          std::memcpy(&lb, &lo, sizeof lb);
-          b |= lb;
-          double d;
-          std::memcpy(&d, &b, sizeof d);
-          return d;
-        };
-        if ((int)n < len) {
-          if ((t & 1) == 0)
-            v = make_double2(a.cpre[0][i0 + c + n], packed(a.xq[0][i0 + n] & 0xFFFFu, (float)n));
-          else
-            v = make_double2(a.cpre[0][i0 + c + a.te[0][i0 + n]], a.tab[i0 + n]);
-        } else if ((int)n == len) {
-          v = (t & 1) == 0 ? make_double2(a.cpre[0][i0 + c + len], packed(0xFFFFu, (float)len))
-                           : make_double2(a.cpre[0][i0 + c + len], 0.0);
-        }
-        et[2 * base + t] = v;
+        et[nq * base + t] = i15_quarter(ht, c, i0, len, (int)n, t % nq, ly.lookback[slot]);
       }
     }
-    std::memcpy(img + ly.sxq, a.xq[0], sizeof(unsigned) << L);
-    std::memcpy(img + ly.ste, a.te[0], (size_t)1 << L);
+    std::memcpy(img + ly.sxq[slot], a.xq[slot], sizeof(unsigned) << L);
+    std::memcpy(img + ly.ste[slot], a.te[slot], (size_t)1 << L);
   }
 }
 

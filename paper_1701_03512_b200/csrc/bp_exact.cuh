@@ -173,24 +173,33 @@ __host__ __device__ inline unsigned i15_map(float vf, float s, float o) {
 // copies it with coalesced 16-byte loads instead of computing the tables.
 __host__ __device__ constexpr size_t align16(size_t v) { return (v + 15) & ~(size_t)15; }
 struct K1SmemLayout {
-  bool i15, need_w;
-  int nt, ng0, ng1;
-  size_t sw, sW1, sW2, sgray0, sgray1, si15, sxq, ste, total;
+  bool need_w;
+  int nt;
+  bool i15[2];            // per table slot: the I15 screen on its big classes
+  bool lookback[2];       // per table slot: a lookback kind (thresholds tie with the table)
+  int ng[2];              // Gray-table groups per slot (I15: only the small classes')
+  size_t sw, sW1, sW2;
+  size_t sgray[2], si15[2], sxq[2], ste[2], total;
 };
 __host__ __device__ constexpr int kind_tables(unsigned km) {
   return (int)((km >> kAC) & 1) + (int)((km >> kAP) & 1) + (int)((km >> kFL) & 1) + (int)((km >> kFLP) & 1);
 }
+#ifndef BP_I15_LOOKBACK
+#define BP_I15_LOOKBACK 1  // the screen on the lookback slots too (branch-free boundary fix)
+#endif
 template <int L>
 __host__ __device__ constexpr K1SmemLayout k1_smem_layout(unsigned km) {
   K1SmemLayout o{};
   o.nt = kind_tables(km);
-  o.i15 = i15_on<L>() && (((km >> kAC) & 1) || ((km >> kAP) & 1));
   o.need_w = ((km >> kFL) & 1) || ((km >> kFLP) & 1);
-  o.ng1 = n_groups(L);
+  // table slots in kind order AC, AP, FL, FLP
+  int kinds[2] = {-1, -1}, t = 0;
+  const int order[4] = {kAC, kAP, kFL, kFLP};
+  for (int i = 0; i < 4; ++i)
+    if (((km >> order[i]) & 1) && t < 2) kinds[t++] = order[i];
   int small = 0;
   for (int c = 0; c <= L; ++c)
     if (!i15_class(L, c)) small += class_groups(L, c);
-  o.ng0 = o.i15 ? small : n_groups(L);
   constexpr int kSlots = 64;  // Gray-table slots per group (kGraySlots, bp_leaf.cuh)
   size_t off = 0;
   o.sw = off;
@@ -199,16 +208,20 @@ __host__ __device__ constexpr K1SmemLayout k1_smem_layout(unsigned km) {
   off += o.need_w ? sizeof(double) * (kMaxN + 2) : 0;
   o.sW2 = off;
   off = align16(off + (o.need_w ? sizeof(double) * (kMaxN + 2) : 0));
-  o.sgray0 = off;
-  off += o.nt > 0 ? (size_t)16 * o.ng0 * kSlots : 0;
-  o.sgray1 = off;
-  off += o.nt > 1 ? (size_t)16 * o.ng1 * kSlots : 0;
-  o.si15 = off;
-  off += o.i15 ? (size_t)32 * i15_entries(L) : 0;
-  o.sxq = off;
-  off += o.i15 ? (size_t)4 << L : 0;
-  o.ste = off;
-  off += o.i15 ? (size_t)1 << L : 0;
+  for (int s = 0; s < 2; ++s) {
+    const bool has = s < o.nt;
+    o.lookback[s] = has && (kinds[s] == kFL || kinds[s] == kFLP);
+    o.i15[s] = has && i15_on<L>() && (!o.lookback[s] || BP_I15_LOOKBACK);
+    o.ng[s] = has ? (o.i15[s] ? small : n_groups(L)) : 0;
+    o.sgray[s] = off;
+    off += (size_t)16 * o.ng[s] * kSlots;
+    o.si15[s] = off;
+    off += o.i15[s] ? (size_t)(o.lookback[s] ? 48 : 32) * i15_entries(L) : 0;  // i15_entry_bytes (bp_leaf.cuh)
+    o.sxq[s] = off;
+    off += o.i15[s] ? (size_t)4 << L : 0;
+    o.ste[s] = off;
+    off = align16(off + (o.i15[s] ? (size_t)1 << L : 0));
+  }
   o.total = align16(off);
   return o;
 }

@@ -76,18 +76,13 @@ k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_
   // of lattice prices that tie with the table values, so those kinds keep the
   // fp64 block.
   constexpr K1SmemLayout LY = k1_smem_layout<L>(KM);
-  constexpr bool I15 = LY.i15;
+  constexpr bool I15 = LY.i15[0] || LY.i15[1];
   constexpr bool needW = LY.need_w;
   static_assert(kGraySlots == 64, "k1_smem_layout assumes 64 Gray slots per group");
   __shared__ __align__(16) unsigned char simg[LY.total];
   double* sw = reinterpret_cast<double*>(simg + LY.sw);
   double* sW1 = reinterpret_cast<double*>(simg + LY.sW1);
   double* sW2 = reinterpret_cast<double*>(simg + LY.sW2);
-  const double2* sgray0 = reinterpret_cast<const double2*>(simg + LY.sgray0);
-  const double2* sgray1 = reinterpret_cast<const double2*>(simg + LY.sgray1);
-  const double2* si15 = reinterpret_cast<const double2*>(simg + LY.si15);
-  const unsigned* sxq = reinterpret_cast<const unsigned*>(simg + LY.sxq);
-  const unsigned char* ste = simg + LY.ste;
   if (ga) {
     const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(ga) + align16(sizeof(ExactArgs<L>)));
     uint4* dst = reinterpret_cast<uint4*>(simg);
@@ -106,24 +101,26 @@ k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_
     }
   } else {
     // no image: build the tables here from the parameter bank
-    double* w_ = reinterpret_cast<double*>(simg + LY.sw);
-    for (int i = threadIdx.x; i < kMaxN + 2 + NC; i += blockDim.x) w_[i] = (i < kMaxN + 2) ? a.w[i] : 0.0;
-    double2* g0 = reinterpret_cast<double2*>(simg + LY.sgray0);
-    double2* g1 = reinterpret_cast<double2*>(simg + LY.sgray1);
-    if constexpr (I15) {
-      gray_fill_small<L, 0>(a.gpre[0], g0);
-      i15_fill<L, 0>(ParamTabs<L, 0>{a}, reinterpret_cast<double2*>(simg + LY.si15));
-      for (int i = threadIdx.x; i < (1 << L); i += blockDim.x) {
-        reinterpret_cast<unsigned*>(simg + LY.sxq)[i] = a.xq[0][i];
-        simg[LY.ste + i] = a.te[0][i];
+    for (int i = threadIdx.x; i < kMaxN + 2 + NC; i += blockDim.x) sw[i] = (i < kMaxN + 2) ? a.w[i] : 0.0;
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      if (t >= NT) break;
+      double2* g = reinterpret_cast<double2*>(simg + LY.sgray[t]);
+      if (LY.i15[t]) {
+        gray_fill_small<L, 0>(a.gpre[t], g);
+        if (t == 0)
+          i15_fill<L, 0>(ParamTabs<L, 0>{a}, reinterpret_cast<double2*>(simg + LY.si15[0]), LY.lookback[0]);
+        else
+          i15_fill<L, 0>(ParamTabs<L, 1>{a}, reinterpret_cast<double2*>(simg + LY.si15[1]), LY.lookback[1]);
+        for (int i = threadIdx.x; i < (1 << L); i += blockDim.x) {
+          reinterpret_cast<unsigned*>(simg + LY.sxq[t])[i] = a.xq[t][i];
+          simg[LY.ste[t] + i] = a.te[t][i];
+        }
+      } else {
+        for (int i = threadIdx.x; i < NG * kGraySlots; i += blockDim.x)
+          g[i] = gray_table_entry(&a.gpre[t][i / kGraySlots][0], (unsigned)(i % kGraySlots), true);
       }
-    } else if constexpr (NT > 0) {
-      for (int i = threadIdx.x; i < NG * kGraySlots; i += blockDim.x)
-        g0[i] = gray_table_entry(&a.gpre[0][i / kGraySlots][0], (unsigned)(i % kGraySlots), true);
     }
-    if constexpr (NT > 1)
-      for (int i = threadIdx.x; i < NG * kGraySlots; i += blockDim.x)
-        g1[i] = gray_table_entry(&a.gpre[1][i / kGraySlots][0], (unsigned)(i % kGraySlots), true);
     if constexpr (needW) {
       __syncthreads();
       // W1[h] = sum_c w[h+c] C(L,c), W2[h] = sum_c w[h+c] C(L,c) e_c (the lookback
@@ -131,15 +128,15 @@ k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_
       for (int i = threadIdx.x; i < kMaxN + 2; i += blockDim.x) {
         double w1 = 0.0, w2 = 0.0;
         for (int c = 0; c < NC; ++c) {
-          w1 = fma(w_[i + c], a.b_cls[c], w1);
-          w2 = fma(w_[i + c] * a.b_cls[c], a.e_cls[c], w2);
+          w1 = fma(sw[i + c], a.b_cls[c], w1);
+          w2 = fma(sw[i + c] * a.b_cls[c], a.e_cls[c], w2);
         }
         sW1[i] = w1;
         sW2[i] = w2;
       }
     }
   }
-#define BP_GTAB(SLOT) reinterpret_cast<const char*>((SLOT) == 0 ? &sgray0[0] : &sgray1[0])
+#define BP_GTAB(SLOT) reinterpret_cast<const char*>(simg + LY.sgray[SLOT])
 #define BP_LEAF(SLOT, GTV, TH) leaf_block_gray<L, NP, SLOT, GTV>(tb, BP_GTAB(SLOT), TH, acc, cnt)
 #else
   // diagnostic configurations (BP_GRAY=0, BP_FOLD=0, BP_TAB_SMEM=1): tables built here
@@ -245,20 +242,23 @@ k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_
       // the class finalisation, node value = sum_c w[h+c] * contrib_c.  Kinds
       // run one after the other so only one kind's accumulators are live.
 #if BP_FOLD
-      // the leaf block of a slot: I15 screen on slot 0 of the Asian kinds
+      // the leaf block of a slot: the I15 screen where the layout puts it (the
+      // lookback slots fix every lane's boundary leaf without a branch)
 #define BP_FOLDLEAF(SLOT, GTV, TH)                                                                            \
-  if constexpr (I15 && (SLOT) == 0)                                                                          \
-    leaf_block_fold_i15<L, SLOT, GTV>(ParamTabs<L, SLOT>{a}, reinterpret_cast<const uint4*>(sxq) + zoff,    \
-                                      I15Ctx{reinterpret_cast<const char*>(si15), sxq, ste,                  \
-                                             1u | (unsigned)sc.zero, {0.f, 0.f}},                           \
-                                      tb, BP_GTAB(SLOT), sw, hn, TH, sA, sN);                                \
+  if constexpr (LY.i15[SLOT])                                                                                \
+    leaf_block_fold_i15<L, SLOT, GTV, LY.lookback[SLOT]>(                                                    \
+        ParamTabs<L, SLOT>{a}, reinterpret_cast<const uint4*>(simg + LY.sxq[SLOT]) + zoff,                   \
+        I15Ctx{reinterpret_cast<const char*>(simg + LY.si15[SLOT]),                                          \
+               reinterpret_cast<const unsigned*>(simg + LY.sxq[SLOT]), simg + LY.ste[SLOT],                 \
+               1u | (unsigned)sc.zero, {0.f, 0.f}},                                                          \
+        tb, BP_GTAB(SLOT), sw, hn, TH, sA, sN);                                                              \
   else                                                                                                       \
     leaf_block_fold<L, NP, SLOT, GTV>(tb, BP_GTAB(SLOT), sw, hn, TH, sA, sN)
       // node value, affine in sA = sum_c w[h+c] A_c and sN = sum_c w[h+c] n_c
       // (A_c / n_c: class-c in-the-money table sum and count):
       //   AC  S sA + base sN              AP  -(S sA + base sN)
       //   FL  S (sA - W2) + Mx (W1 - sN)  FLP K sN - S sA + max(K - Mn, 0) (W1 - sN)
-      if (kAC_ || kAP_) {
+      if constexpr (kAC_ || kAP_) {
         double sA[NP], sN[NP];
         if constexpr (kAC_) {
           BP_FOLDLEAF(slotAC, true, thC);
@@ -272,14 +272,14 @@ k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_
           else comp_add(ts[kAP], tc[kAP], -v);
         }
       }
-      if (kFL_) {
+      if constexpr (kFL_) {
         double sA[NP], sN[NP];
         BP_FOLDLEAF(slotFL, true, thX);
 #pragma unroll
         for (int p = 0; p < NP; ++p)
           comp_add(ts[kFL], tc[kFL], fma(Sn[p], sA[p] - sW2[hn[p]], Mxn[p] * (sW1[hn[p]] - sN[p])));
       }
-      if (kFLP_) {
+      if constexpr (kFLP_) {
         double sA[NP], sN[NP];
         BP_FOLDLEAF(slotFLP, false, thN);
 #pragma unroll
@@ -315,7 +315,7 @@ k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_
           comp_add(ts[kAP], tc[kAP], v);
         }
       }
-      if (kFL_) {
+      if constexpr (kFL_) {
         double acc[NP][NC];
         int cnt[NP][NC];
         zero_acc<NP, NC>(acc, cnt);
@@ -333,7 +333,7 @@ k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_
           comp_add(ts[kFL], tc[kFL], v);
         }
       }
-      if (kFLP_) {
+      if constexpr (kFLP_) {
         double acc[NP][NC];
         int cnt[NP][NC];
         zero_acc<NP, NC>(acc, cnt);

@@ -244,7 +244,11 @@ struct I15Ctx {
   unsigned one;         // 1, opaque to the compiler (keeps the multiply-add an IMAD)
   float thf[2];         // node thresholds in fp32
 };
-constexpr int kI15Entry = 32;  // bytes per entry
+// bytes per entry: Asian slots {P[n'], n' | x~_n'}, {P[m], x_n'} (the rare fix
+// reads m and x~_m from the tie-run and code arrays); lookback slots, whose
+// fix runs for nearly every node, carry {P[n'], n' | x~_n'}, {P[m], m},
+// {x_n', x~_m} so it needs no dependent loads
+__host__ __device__ constexpr int i15_entry_bytes(bool lookback) { return lookback ? 48 : 32; }
 #ifndef BP_I15_WAYS
 #define BP_I15_WAYS 1  // r2 scan: 1 (no partials) best at 3 CTAs/SM, equal at 2
 #endif
@@ -262,27 +266,27 @@ __host__ __device__ constexpr int ctz_c(int v) {
 template <int L, int SLOT>
 struct ParamTabs {
   const ExactArgs<L>& a;
-  __device__ __forceinline__ float nrm_s(int c) const { return a.nrm_s[SLOT][c]; }
-  __device__ __forceinline__ float nrm_o(int c) const { return a.nrm_o[SLOT][c]; }
-  __device__ __forceinline__ double tab(int i) const { return a.tab[SLOT * (1 << L) + i]; }
-  __device__ __forceinline__ double cpre(int i) const { return a.cpre[SLOT][i]; }
-  __device__ __forceinline__ unsigned xq(int i) const { return a.xq[SLOT][i]; }
-  __device__ __forceinline__ unsigned te(int i) const { return a.te[SLOT][i]; }
+  __host__ __device__ __forceinline__ float nrm_s(int c) const { return a.nrm_s[SLOT][c]; }
+  __host__ __device__ __forceinline__ float nrm_o(int c) const { return a.nrm_o[SLOT][c]; }
+  __host__ __device__ __forceinline__ double tab(int i) const { return a.tab[SLOT * (1 << L) + i]; }
+  __host__ __device__ __forceinline__ double cpre(int i) const { return a.cpre[SLOT][i]; }
+  __host__ __device__ __forceinline__ unsigned xq(int i) const { return a.xq[SLOT][i]; }
+  __host__ __device__ __forceinline__ unsigned te(int i) const { return a.te[SLOT][i]; }
 };
 struct SmemTabs {
   const float *ns, *no;
   const double *tb, *cp;
   const unsigned* xw;
   const unsigned char* tw;
-  __device__ __forceinline__ float nrm_s(int c) const { return ns[c]; }
-  __device__ __forceinline__ float nrm_o(int c) const { return no[c]; }
-  __device__ __forceinline__ double tab(int i) const { return tb[i]; }
-  __device__ __forceinline__ double cpre(int i) const { return cp[i]; }
-  __device__ __forceinline__ unsigned xq(int i) const { return xw[i]; }
-  __device__ __forceinline__ unsigned te(int i) const { return tw[i]; }
+  __host__ __device__ __forceinline__ float nrm_s(int c) const { return ns[c]; }
+  __host__ __device__ __forceinline__ float nrm_o(int c) const { return no[c]; }
+  __host__ __device__ __forceinline__ double tab(int i) const { return tb[i]; }
+  __host__ __device__ __forceinline__ double cpre(int i) const { return cp[i]; }
+  __host__ __device__ __forceinline__ unsigned xq(int i) const { return xw[i]; }
+  __host__ __device__ __forceinline__ unsigned te(int i) const { return tw[i]; }
 };
 
-template <int L, int SLOT, bool GT, int C, class TS>
+template <int L, int SLOT, bool GT, int C, class TS, bool FIXALL = false>
 struct I15Class {
   static constexpr int len = binom(L, C), nb = bit_length(len), i0 = class_start(L, C);
   static __device__ __forceinline__ void run(const TS& a, const uint4* __restrict__ xb, const I15Ctx& x,
@@ -321,16 +325,22 @@ struct I15Class {
     for (int b = nb - 1; b >= 0; --b) c1 = __funnelshift_l(g[b], c1, 1);
 #pragma unroll
     for (int b = 0; b < nb; ++b) c0 += (g[b] & 0x8000u) << b;
-    const char* et0 = x.etab + i15_base(L, C) * kI15Entry + (c0 >> 10);
-    const char* et1 = x.etab + i15_base(L, C) * kI15Entry + (c1 << 5);
+    constexpr int EB = i15_entry_bytes(FIXALL);
+    const char* et0 = x.etab + i15_base(L, C) * EB + (EB / 16) * (c0 >> 11);
+    const char* et1 = x.etab + i15_base(L, C) * EB + (EB / 16) * (c1 << 4);
     const double2 e0 = *reinterpret_cast<const double2*>(et0);
     const double2 e1 = *reinterpret_cast<const double2*>(et1);
     double2 r0 = make_double2(e0.x, (double)__int_as_float(__double2loint(e0.y)));
     double2 r1 = make_double2(e1.x, (double)__int_as_float(__double2loint(e1.y)));
     const bool amb0 = (unsigned)__double2hiint(e0.y) == k0, amb1 = (unsigned)__double2hiint(e1.y) == k1;
-    // warp-uniform branch (the surrounding control flow stays uniform; K3 may
-    // run partial warps on tiny trees, hence the active mask)
-    if (__any_sync(__activemask(), amb0 || amb1)) {
+    if constexpr (FIXALL) {
+      // lookback kinds: nearly every node has a threshold tie in the class,
+      // so every lane settles its boundary leaf without a branch
+      fix_all(a, x, et0, th[0], k0, amb0, r0);
+      fix_all(a, x, et1, th[1], k1, amb1, r1);
+    } else if (__any_sync(__activemask(), amb0 || amb1)) {
+      // warp-uniform branch (the surrounding control flow stays uniform; K3 may
+      // run partial warps on tiny trees, hence the active mask)
       fix(a, x, et0, th[0], k0, amb0, r0);
       fix(a, x, et1, th[1], k1, amb1, r1);
     }
@@ -339,15 +349,25 @@ struct I15Class {
     A[1] = r1.x;
     n[1] = r1.y;
   }
+  // fix without branches: loads and selects for every lane, the walk only
+  // for a lane whose tie run ends on another leaf with the threshold's code
+  static __device__ __forceinline__ void fix_all(const TS& a, const I15Ctx& x, const char* et, double th,
+                                                 unsigned k, bool amb, double2& r) {
+    const double2 q1 = *reinterpret_cast<const double2*>(et + 16);  // {P_c[m], m}
+    const double2 q2 = *reinterpret_cast<const double2*>(et + 32);  // {x_n', x~_m}
+    const bool itm = amb && (GT ? q2.x > th : q2.x < th);
+    if (itm) r = q1;
+    if (itm && (unsigned)__double2loint(q2.y) == k) r = walk(a, x, th, k, (int)q1.y);
+  }
   // leaf n' in fp64 from the entry (with its tie run); a further leaf with
   // the threshold's screened value takes the exact walk
   static __device__ __forceinline__ void fix(const TS& a, const I15Ctx& x, const char* et, double th,
                                              unsigned k, bool amb, double2& r) {
     if (!amb) return;
-    const double2 e1 = *reinterpret_cast<const double2*>(et + 16);  // {P_c[m], x_n'}
-    if (GT ? e1.y > th : e1.y < th) {
+    const double2 q1 = *reinterpret_cast<const double2*>(et + 16);  // {P_c[m], x_n'}
+    if (GT ? q1.y > th : q1.y < th) {
       const int m = x.ste[i0 + (int)r.y];
-      r = make_double2(e1.x, (double)m);
+      r = make_double2(q1.x, (double)m);
       if (m < len && (x.sxq[i0 + m] & 0xFFFFu) == k) r = walk(a, x, th, k, m);
     }
   }
@@ -363,7 +383,7 @@ struct I15Class {
 
 // K1 leaf block with the I15 screen on the big classes and the Gray fp64
 // block (FoldGroups) on the others; per class the fold as leaf_block_fold.
-template <int L, int SLOT, bool GT, int C, class TS>
+template <int L, int SLOT, bool GT, int C, class TS, bool FIXALL = false>
 struct FoldClassesI15 {
   static __device__ __forceinline__ void run(const TS& a, const uint4* __restrict__ xb, const I15Ctx& x,
                                              const double2* __restrict__ tb, const char* __restrict__ gtab,
@@ -372,7 +392,7 @@ struct FoldClassesI15 {
     if constexpr (C <= L) {
       double A[2], n[2];
       if constexpr (i15_class(L, C))
-        I15Class<L, SLOT, GT, C, TS>::run(a, xb, x, th, A, n);
+        I15Class<L, SLOT, GT, C, TS, FIXALL>::run(a, xb, x, th, A, n);
       else
         FoldGroups<L, 2, SLOT, GT, C, 0, true>::run(tb, gtab, th, A, n);
 #pragma unroll
@@ -381,12 +401,12 @@ struct FoldClassesI15 {
         sA[p] = C == 0 ? w * A[p] : fma(w, A[p], sA[p]);
         sN[p] = C == 0 ? w * n[p] : fma(w, n[p], sN[p]);
       }
-      FoldClassesI15<L, SLOT, GT, C + 1, TS>::run(a, xb, x, tb, gtab, sw, hn, th, sA, sN);
+      FoldClassesI15<L, SLOT, GT, C + 1, TS, FIXALL>::run(a, xb, x, tb, gtab, sw, hn, th, sA, sN);
     }
   }
 };
 
-template <int L, int SLOT, bool GT, class TS>
+template <int L, int SLOT, bool GT, bool FIXALL = false, class TS>
 __device__ __forceinline__ void leaf_block_fold_i15(const TS& a, const uint4* __restrict__ xb, I15Ctx x,
                                                     const double2* __restrict__ tb,
                                                     const char* __restrict__ gtab, const double* __restrict__ sw,
@@ -394,7 +414,33 @@ __device__ __forceinline__ void leaf_block_fold_i15(const TS& a, const uint4* __
                                                     double (&sN)[2]) {
   x.thf[0] = __double2float_rn(th[0]);
   x.thf[1] = __double2float_rn(th[1]);
-  FoldClassesI15<L, SLOT, GT, 0, TS>::run(a, xb, x, tb, gtab, sw, hn, th, sA, sN);
+  FoldClassesI15<L, SLOT, GT, 0, TS, FIXALL>::run(a, xb, x, tb, gtab, sw, hn, th, sA, sN);
+}
+
+// Quarter q of the entry for count n of class c (positions i0 .. i0+len),
+// m = te(n), x~ of position len = 0xFFFF (never equal to a threshold):
+//   Asian (32 B):    0 {P_c[n], n (fp32 bits) | x~_n << 32}, 1 {P_c[m], x_n}
+//   lookback (48 B): 0 as above, 1 {P_c[m], m}, 2 {x_n, x~_m}
+template <class TS>
+__host__ __device__ inline double2 i15_quarter(const TS& a, int c, int i0, int len, int n, int q, bool lookback) {
+  auto packed = [](unsigned hi, unsigned lo) {
+    const unsigned long long b = ((unsigned long long)hi << 32) | lo;
+    double d;
+    memcpy(&d, &b, sizeof d);
+    return d;
+  };
+  if (n > len) return make_double2(0.0, 0.0);
+  const int m = n < len ? (int)a.te(i0 + n) : len;
+  const unsigned xq_n = n < len ? (a.xq(i0 + n) & 0xFFFFu) : 0xFFFFu;
+  const unsigned xq_m = m < len ? (a.xq(i0 + m) & 0xFFFFu) : 0xFFFFu;
+  const double x_n = n < len ? a.tab(i0 + n) : 0.0;
+  float nf = (float)n;
+  unsigned nb;
+  memcpy(&nb, &nf, sizeof nb);
+  if (q == 0) return make_double2(a.cpre(i0 + c + n), packed(xq_n, nb));
+  if (!lookback) return make_double2(a.cpre(i0 + c + m), x_n);
+  if (q == 1) return make_double2(a.cpre(i0 + c + m), (double)m);
+  return make_double2(x_n, packed(0u, xq_m));
 }
 
 // The slot's entry table, class by class (compile-time class layout): entry
@@ -402,28 +448,18 @@ __device__ __forceinline__ void leaf_block_fold_i15(const TS& a, const uint4* __
 // {P_c[n], n (fp32 bits) | x~_n << 32} and {P_c[te(n)], x_n}
 // (x~_|c| = 0xFFFF: never equal to a threshold).
 template <int L, int C, class TS>
-__device__ inline void i15_fill(const TS& a, double2* __restrict__ et) {
+__device__ inline void i15_fill(const TS& a, double2* __restrict__ et, bool lookback) {
   if constexpr (C <= L) {
     if constexpr (i15_class(L, C)) {
       constexpr int len = binom(L, C), i0 = class_start(L, C), base = i15_base(L, C), slots = i15_slots(L, C);
-      for (int t = threadIdx.x; t < 2 * slots; t += blockDim.x) {
-        unsigned n = (unsigned)(t >> 1);
+      const int nq = i15_entry_bytes(lookback) / 16;
+      for (int t = threadIdx.x; t < nq * slots; t += blockDim.x) {
+        unsigned n = (unsigned)(t / nq);
         for (int sh = 1; sh < 16; sh <<= 1) n ^= n >> sh;  // Gray -> binary
-        double2 v = make_double2(0.0, 0.0);
-        if ((int)n < len) {
-          if ((t & 1) == 0)
-            v = make_double2(a.cpre(i0 + C + n),
-                             __hiloint2double((int)(a.xq(i0 + n) & 0xFFFFu), __float_as_int((float)n)));
-          else
-            v = make_double2(a.cpre(i0 + C + a.te(i0 + n)), a.tab(i0 + n));
-        } else if ((int)n == len) {
-          v = (t & 1) == 0 ? make_double2(a.cpre(i0 + C + len), __hiloint2double(0xFFFF, __float_as_int((float)len)))
-                           : make_double2(a.cpre(i0 + C + len), 0.0);
-        }
-        et[2 * base + t] = v;
+        et[nq * base + t] = i15_quarter(a, C, i0, len, (int)n, t % nq, lookback);
       }
     }
-    i15_fill<L, C + 1, TS>(a, et);
+    i15_fill<L, C + 1, TS>(a, et, lookback);
   }
 }
 
