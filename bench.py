@@ -380,15 +380,12 @@ I15_SHARE_L8 = 238.0 / 256.0  # leaves of the up-count classes with >= 16 leaves
 
 def leaf_test_mix(kinds):
     """(form, tests per path) of K1's leaf tests for the workload's kinds:
-    the Asian kinds screen their big classes (I15) and test the rest in fp64;
-    the lookback kinds test every leaf in fp64 (csrc/bp_exact_fast.cuh)."""
+    every table kind (Asian and lookback) screens its big up-count classes
+    (I15) and tests the small classes in fp64 (csrc/bp_exact_fast.cuh)."""
     mix = {"fp64": 0.0, "i15": 0.0}
-    for k in kinds:
-        if k in ("asian-call", "asian-put"):
-            mix["i15"] += I15_SHARE_L8
-            mix["fp64"] += 1.0 - I15_SHARE_L8
-        else:
-            mix["fp64"] += 1.0
+    for _ in kinds:
+        mix["i15"] += I15_SHARE_L8
+        mix["fp64"] += 1.0 - I15_SHARE_L8
     return mix
 
 
@@ -597,11 +594,11 @@ def run_ours(args):
         "impl_detail": {"parallelism": f"superblock-shard x{world} (one rank per GPU, NCCL all_gather)",
                         "l2": "flushed (256 MiB write) between timed steps",
                         "engine": "affine-threshold" if sh.engine else "path-walk", "inner_bits": sh.inner_bits,
-                        "superblocks": sh.n_sb, "leaf_block": "Asian kinds: 15-bit integer screen of the "
-                                                             "big classes (two nodes per IMAD, Gray-code counters, "
-                                                             "fp64 boundary leaf); lookback kinds and small classes: "
-                                                             "fp64 compares with Gray-code predicate counting; "
-                                                             "per-class fold, 2 nodes per table load"},
+                        "superblocks": sh.n_sb, "leaf_block": "15-bit integer screen of the big up-count "
+                                                             "classes (two nodes per IMAD, Gray-code counters, fp64 "
+                                                             "boundary leaf); small classes: fp64 compares with "
+                                                             "Gray-code predicate counting; per-class fold, 2 nodes "
+                                                             "per table load"},
         "values": vals, "config3": extra or None, **extra45, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clocks,
