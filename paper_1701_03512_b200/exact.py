@@ -103,6 +103,8 @@ def tree_of(req):
 
 
 ENGINES = {0: "path-walk", 1: "affine-threshold", 2: "threshold-search", 3: "affine-threshold-weighted"}
+_DEV_ARRAYS: dict = {}  # device tuple -> ctypes int array (read-only once built)
+_MASK_BITS: dict = {}   # payoff mask -> its bits in ascending order
 
 
 def value_exact(req, kinds: Optional[Sequence] = None, devices: Optional[Sequence[int]] = None,
@@ -121,15 +123,20 @@ def value_exact(req, kinds: Optional[Sequence] = None, devices: Optional[Sequenc
     for k in kinds:
         mask |= 1 << kind_bit(k)
     tree, keep = tree_of(req)
-    devs = list(devices) if devices is not None else _devices(req)
-    arr = (ctypes.c_int * len(devs))(*devs)
+    devs = tuple(devices) if devices is not None else tuple(_devices(req))
+    arr = _DEV_ARRAYS.get(devs)
+    if arr is None:
+        arr = _DEV_ARRAYS.setdefault(devs, (ctypes.c_int * len(devs))(*devs))
     res = _native.BpExactResult()
     flags = ((_native.FLAG_COUNT if count else 0) | (_native.FLAG_GENERIC if generic else 0)
              | (_native.FLAG_THRESHOLD if search else 0))
     L = _native.lib()
     _native.check(L.bp_exact(ctypes.byref(tree), mask, flags, len(devs), arr, ctypes.byref(res)))
     del keep
-    vals = {BIT_TAG[b]: float(res.value[b]) for b in range(_native.N_PAYOFFS) if (mask >> b) & 1}
+    bits = _MASK_BITS.get(mask)
+    if bits is None:
+        bits = _MASK_BITS.setdefault(mask, tuple(b for b in range(_native.N_PAYOFFS) if (mask >> b) & 1))
+    vals = {BIT_TAG[b]: res.value[b] for b in bits}
     hist = np.array(res.hist[: req.inputs.N + 1], dtype=np.uint64) if count else None
     return ExactResult(values=vals, leaves=int(res.leaves), code_sum=int(res.code_sum), hist=hist,
                        kernel_ms=float(res.kernel_ms), engine=ENGINES[int(res.engine)],
