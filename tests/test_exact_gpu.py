@@ -289,3 +289,25 @@ def test_graph_replay_is_bitwise_the_launch_path():
     assert runs["1"] == runs["0"]
     r = runs["1"]
     assert r[0] == r[1] == r[2] == r[6] == r[7] == r[8] and r[3] == r[4] == r[5] and r[0] != r[3]
+
+
+@pytest.mark.parametrize("u", [1.0 + 1e-7, 1.0 + 1e-4, 1.6])
+def test_screen_code_collisions_vs_oracle(u):
+    """Stress of the I15 screen's exact fallback (bp_leaf.cuh I15Class): at
+    u = 1 + 1e-7 every class's values fit in a few 15-bit codes, so nearly
+    every threshold shares a code with many leaves and the boundary fix and
+    the walk decide most leaves in fp64; at u = 1.6 the classes span a wide
+    range.  Every kind, K around the money so thresholds fall inside the
+    classes; K1 against the oracle and against the path walk (1e-12)."""
+    N, S0 = 18, 100.0
+    d = 1.0 / u
+    for K in (99.99, 100.0, 100.02, 140.0):
+        req = _req(N, S0, K, 0.01, 1.0, u, d, 0.5)
+        kinds = [bp.resolve_kind(k) for k in ALL]
+        res = bp.value_exact(req, kinds=kinds)
+        assert res.engine == "affine-threshold"
+        walk = bp.value_exact(req, kinds=kinds, generic=True)
+        want = oracle.exact(N, S0, K, u, d, 0.5, math.exp(-0.01), ALL, workers=16)
+        for k in ALL:
+            assert _close(res.values[k], want[k]), (u, K, k, res.values[k], want[k])
+            assert _close(res.values[k], walk.values[k]), (u, K, k, res.values[k], walk.values[k])
