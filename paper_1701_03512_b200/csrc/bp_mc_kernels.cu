@@ -240,8 +240,11 @@ struct ShiftedSums {
 
 // ---------------------------------------------------------------------------
 // K4/K5: one CTA per work item (grid-stride).  item -> (rep k, stratum m, first draw)
+#ifndef BP_MC_MINB
+#define BP_MC_MINB 1  // resident CTAs per SM targeted by K4 (1: no register cap)
+#endif
 template <unsigned KIND, bool CONSTP>
-__global__ void __launch_bounds__(kMcThreads)
+__global__ void __launch_bounds__(kMcThreads, BP_MC_MINB)
 k_mc_strata(const __grid_constant__ McArgs a, const unsigned long long* __restrict__ draws,
             const unsigned long long* __restrict__ item_stratum, const unsigned long long* __restrict__ item_first,
             unsigned long long items_per_rep, int n_reps, double* __restrict__ item_out) {
