@@ -375,21 +375,26 @@ def fp64_peak(dev):
 # tests; the I15 screen's packed IMAD (two nodes' 15-bit lanes per 32-bit
 # lane) at 0.5 warp-instructions/clk -> 32 leaf tests.
 TESTS_PER_CLK_SMSP = {"fp64": 16.0, "i15": 32.0}
-I15_SHARE_L8 = 238.0 / 256.0  # leaves of the up-count classes with >= 16 leaves (L = 8): the screened ones
 
 
-def leaf_test_mix(kinds):
+def i15_share(L):
+    """Share of an inner block's 2^L leaves in up-count classes with >= 16
+    leaves (the screened ones; csrc/bp_exact.cuh i15_class)."""
+    return sum(math.comb(L, c) for c in range(L + 1) if math.comb(L, c) >= 16) / float(1 << L)
+
+
+def leaf_test_mix(kinds, L):
     """(form, tests per path) of K1's leaf tests for the workload's kinds:
     every table kind (Asian and lookback) screens its big up-count classes
     (I15) and tests the small classes in fp64 (csrc/bp_exact_fast.cuh)."""
     mix = {"fp64": 0.0, "i15": 0.0}
     for _ in kinds:
-        mix["i15"] += I15_SHARE_L8
-        mix["fp64"] += 1.0 - I15_SHARE_L8
+        mix["i15"] += i15_share(L)
+        mix["fp64"] += 1.0 - i15_share(L)
     return mix
 
 
-def roofline(w, workload, k_ms, paths, sm_count, clk, dev):
+def roofline(w, workload, k_ms, paths, sm_count, clk, dev, inner_bits=9):
     """Compare roofline of the dominant kernel (K1, with K2 inside k_ms).
 
     The algorithmic unit is the leaf test (one explicit compare per leaf per
@@ -407,7 +412,7 @@ def roofline(w, workload, k_ms, paths, sm_count, clk, dev):
     mhz = (clk or {}).get("sm_mhz") or k7_mhz
     hz = mhz * 1e6
     tests = paths * len(w["kinds"])
-    mix = leaf_test_mix(w["kinds"])
+    mix = leaf_test_mix(w["kinds"], inner_bits)
     # seconds per path at the compare peak, per form
     sec_per_path = sum(share / (TESTS_PER_CLK_SMSP[f] * 4 * sm_count * hz) for f, share in mix.items())
     peak = len(w["kinds"]) / sec_per_path  # leaf tests / s
@@ -572,7 +577,7 @@ def run_ours(args):
     rank_paths = total_paths * count // n_sb
     k_ms = ms_local if world == 1 else detail["kernel_ms"]
     sm_count = torch.cuda.get_device_properties(dev).multi_processor_count
-    roof = roofline(w, args.workload, k_ms, rank_paths, sm_count, clocks, dev)
+    roof = roofline(w, args.workload, k_ms, rank_paths, sm_count, clocks, dev, sh.inner_bits)
     roof["kernel_ms_source"] = ("mean of the timed steps (K1 + K2, CUDA events on the launch stream)" if world == 1
                                 else "rank 0's super-blocks alone (K1 + K2, CUDA events), no exchange")
 

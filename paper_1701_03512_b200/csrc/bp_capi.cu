@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <list>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -100,11 +101,15 @@ static bool constant_p(const bp_tree* t) {
 // layout: a pure function of (N, engine) so every device count and every
 // machine uses the same decomposition (bitwise reproducibility across G).
 // inner block bits of the fast engine (8 or 9; BINPATHS_INNER_BITS overrides)
+// 9 since the I15 screen: its per-class work amortizes over bigger classes
+// (config 2: 0.168 -> 0.146 ms, config 3: 4.12 -> 3.36 ms); 10 was measured
+// slower (0.232 / 6.2 ms: the unrolled classes outgrow the instruction cache;
+// profiles/r2_scan_inner_bits.log)
 static int fast_L() {
   static int L = [] {
     const char* e = std::getenv("BINPATHS_INNER_BITS");
-    const int v = e ? std::atoi(e) : 8;
-    return (v == 8 || v == 9) ? v : 8;
+    const int v = e ? std::atoi(e) : 9;
+    return (v == 8 || v == 9) ? v : 9;
   }();
   return L;
 }
@@ -267,7 +272,7 @@ static void kind_table_layout(int kind, const std::vector<double>& c, const std:
 // screened value of every position in both 16-bit lanes, and the class
 // prefix sums in sorted order (compensated, rounded once).
 template <int L>
-static void i15_layout(int kind, const double* pos, ExactArgs<L>& a, int slot) {
+static void i15_layout(int kind, const double* pos, ExactArgs<L>& a, ExactTables<L>& tb, int slot) {
   const bool desc = (kind == kAC || kind == kFL);
   for (int c = 0; c <= L; ++c) {
     a.nrm_s[slot][c] = 1.0f;
@@ -295,15 +300,15 @@ static void i15_layout(int kind, const double* pos, ExactArgs<L>& a, int slot) {
       int e = j + 1;
       const double tol = std::ldexp(std::fabs(pos[i0 + j]), -44);
       while (e < len && std::fabs(pos[i0 + e] - pos[i0 + j]) <= tol) ++e;
-      a.te[slot][i0 + j] = (unsigned char)e;
+      tb.te[slot][i0 + j] = (unsigned char)e;
     }
     double sum = 0.0, comp = 0.0;
-    a.cpre[slot][i0 + c] = 0.0;
+    tb.cpre[slot][i0 + c] = 0.0;
     for (int j = 0; j < len; ++j) {
       const unsigned k = i15_map((float)pos[i0 + j], a.nrm_s[slot][c], a.nrm_o[slot][c]);
-      a.xq[slot][i0 + j] = k | (k << 16);
+      tb.xq[slot][i0 + j] = k | (k << 16);
       comp_add(sum, comp, pos[i0 + j]);
-      a.cpre[slot][i0 + c + j + 1] = sum + comp;
+      tb.cpre[slot][i0 + c + j + 1] = sum + comp;
     }
   }
 }
@@ -312,18 +317,19 @@ static void i15_layout(int kind, const double* pos, ExactArgs<L>& a, int slot) {
 template <int L>
 struct HostTabs {
   const ExactArgs<L>& a;
+  const ExactTables<L>& tb;
   int slot;
   __host__ __device__ double tab(int i) const { return a.tab[slot * (1 << L) + i]; }
-  __host__ __device__ double cpre(int i) const { return a.cpre[slot][i]; }
-  __host__ __device__ unsigned xq(int i) const { return a.xq[slot][i]; }
-  __host__ __device__ unsigned te(int i) const { return a.te[slot][i]; }
+  __host__ __device__ double cpre(int i) const { return tb.cpre[slot][i]; }
+  __host__ __device__ unsigned xq(int i) const { return tb.xq[slot][i]; }
+  __host__ __device__ unsigned te(int i) const { return tb.te[slot][i]; }
 };
 
 // K1's shared-memory image (k1_smem_layout), appended to the argument block:
 // the tables every CTA used to build from the parameter bank, built once here
 // with the same formulas (kernel fallback: bp_exact_fast.cuh, ga == nullptr).
 template <int L>
-static void build_smem_image(const ExactArgs<L>& a, unsigned km, unsigned char* img) {
+static void build_smem_image(const ExactArgs<L>& a, const ExactTables<L>& tb, unsigned km, unsigned char* img) {
   const K1SmemLayout ly = k1_smem_layout<L>(km);
   std::memset(img, 0, ly.total);
   constexpr int NC = L + 1, NG = n_groups(L);
@@ -348,7 +354,7 @@ static void build_smem_image(const ExactArgs<L>& a, unsigned km, unsigned char* 
       if (small_only && i15_class(L, c)) continue;
       for (int g = 0; g < class_groups(L, c); ++g, ++k)
         for (int sl = 0; sl < kGraySlots; ++sl)
-          dst[k * kGraySlots + sl] = gray_table_entry(&a.gpre[slot][group_base(L, c) + g][0], (unsigned)sl, true);
+          dst[k * kGraySlots + sl] = gray_table_entry(&tb.gpre[slot][group_base(L, c) + g][0], (unsigned)sl, true);
     }
     (void)NG;
   };
@@ -356,7 +362,7 @@ static void build_smem_image(const ExactArgs<L>& a, unsigned km, unsigned char* 
     gray_groups(slot, reinterpret_cast<double2*>(img + ly.sgray[slot]), ly.i15[slot]);
     if (!ly.i15[slot]) continue;
     double2* et = reinterpret_cast<double2*>(img + ly.si15[slot]);
-    const HostTabs<L> ht{a, slot};
+    const HostTabs<L> ht{a, tb, slot};
     for (int c = 0; c <= L; ++c) {
       if (!i15_class(L, c)) continue;
       const int len = binom(L, c), i0 = class_start(L, c), base = i15_base(L, c), slots = i15_slots(L, c);
@@ -367,8 +373,8 @@ static void build_smem_image(const ExactArgs<L>& a, unsigned km, unsigned char* 
         et[nq * base + t] = i15_quarter(ht, c, i0, len, (int)n, t % nq, ly.lookback[slot]);
       }
     }
-    std::memcpy(img + ly.sxq[slot], a.xq[slot], sizeof(unsigned) << L);
-    std::memcpy(img + ly.ste[slot], a.te[slot], (size_t)1 << L);
+    std::memcpy(img + ly.sxq[slot], tb.xq[slot], sizeof(unsigned) << L);
+    std::memcpy(img + ly.ste[slot], tb.te[slot], (size_t)1 << L);
   }
 }
 
@@ -376,6 +382,9 @@ template <int L>
 static int fill_fast_args(const bp_tree* t, const Layout& lay, unsigned km, std::vector<unsigned char>& buf) {
   buf.assign(sizeof(ExactArgs<L>), 0);
   ExactArgs<L>& a = *reinterpret_cast<ExactArgs<L>*>(buf.data());
+  auto tables = std::make_unique<ExactTables<L>>();  // setup-only tables (device image)
+  ExactTables<L>& tbl = *tables;
+  std::memset(&tbl, 0, sizeof(tbl));
   std::vector<double> c, mx, mn, e;
   std::vector<int> h;
   build_inner(L, t->u, t->d, c, mx, mn, e, h);
@@ -387,9 +396,9 @@ static int fill_fast_args(const bp_tree* t, const Layout& lay, unsigned km, std:
   const int nt = (int)kinds.size();
   std::vector<double> pos(1 << L);
   for (int slot = 0; slot < nt; ++slot) {
-    kind_table_layout<L>(kinds[slot], c, mx, mn, pos.data(), a.gpre[slot]);
+    kind_table_layout<L>(kinds[slot], c, mx, mn, pos.data(), tbl.gpre[slot]);
     for (int i = 0; i < (1 << L); ++i) a.tab[slot * (1 << L) + i] = pos[i];
-    if constexpr (i15_on<L>()) i15_layout<L>(kinds[slot], pos.data(), a, slot);
+    if constexpr (i15_on<L>()) i15_layout<L>(kinds[slot], pos.data(), a, tbl, slot);
   }
   // middle tables (chunk of m steps)
   const int m = lay.m;
@@ -438,10 +447,13 @@ static int fill_fast_args(const bp_tree* t, const Layout& lay, unsigned km, std:
   s.n_mid = 1 << m;
   s.q = lay.q;
   s.zero = 0;
-  // the shared-memory image after the block (K1's CTA setup copies it)
+  // the device image after the block: the shared-memory image (K1's CTA
+  // setup copies it), then the class prefix sums (the exact walk reads them)
   const size_t head = align16(sizeof(ExactArgs<L>));
-  buf.resize(head + k1_smem_layout<L>(km).total, 0);
-  build_smem_image<L>(*reinterpret_cast<ExactArgs<L>*>(buf.data()), km, buf.data() + head);
+  const size_t simg = k1_smem_layout<L>(km).total;
+  buf.resize(head + simg + sizeof(double) * cpre_doubles<L>(), 0);
+  build_smem_image<L>(*reinterpret_cast<ExactArgs<L>*>(buf.data()), tbl, km, buf.data() + head);
+  std::memcpy(buf.data() + head + simg, &tbl.cpre[0][0], sizeof(double) * cpre_doubles<L>());
   return BP_OK;
 }
 
@@ -546,9 +558,13 @@ struct FastArgsKey {
   }
 };
 
+// the scalars of an argument block of inner block size L
+static ExactScalars* exact_scalars(std::vector<unsigned char>& buf, int L) {
+  return L == 8 ? &reinterpret_cast<ExactArgs<8>*>(buf.data())->s : &reinterpret_cast<ExactArgs<9>*>(buf.data())->s;
+}
+
 static void set_contract(std::vector<unsigned char>& buf, int L, const bp_tree* t) {
-  ExactScalars* s = (L == 8) ? &reinterpret_cast<ExactArgs<8>*>(buf.data())->s
-                             : &reinterpret_cast<ExactArgs<9>*>(buf.data())->s;
+  ExactScalars* s = exact_scalars(buf, L);
   s->S0 = t->S0;
   s->K = t->K;
   s->NK = (double)t->n_steps * t->K;
@@ -620,8 +636,7 @@ static void set_units_w(std::vector<unsigned char>& buf, unsigned long long u0, 
 }
 
 static void set_units(std::vector<unsigned char>& buf, int L, unsigned long long u0, unsigned long long u1) {
-  ExactScalars* s = (L == 8) ? &reinterpret_cast<ExactArgs<8>*>(buf.data())->s
-                             : &reinterpret_cast<ExactArgs<9>*>(buf.data())->s;
+  ExactScalars* s = exact_scalars(buf, L);
   s->unit_first = u0;
   s->unit_end = u1;
 }

@@ -126,7 +126,7 @@ static_assert(BP_NP == 1 || BP_NP == 2 || BP_NP == 4, "BP_NP must be 1, 2 or 4")
 constexpr int kI15Min = 16;
 template <int L>
 __host__ __device__ constexpr bool i15_on() {
-  return BP_I15 && BP_FOLD && BP_GRAY && L == 8 && kNodesPerBlock == 2;
+  return BP_I15 && BP_FOLD && BP_GRAY && (L == 8 || L == 9) && kNodesPerBlock == 2;
 }
 __host__ __device__ constexpr bool i15_class(int L, int c) { return binom(L, c) >= kI15Min; }
 __host__ __device__ constexpr int bit_length(int v) {
@@ -226,31 +226,42 @@ __host__ __device__ constexpr K1SmemLayout k1_smem_layout(unsigned km) {
   return o;
 }
 
+// K1's kernel parameter block: what the leaf loops read with uniform loads.
+// The tables only the CTA setup or the rare exact walk need live in the
+// device image after it (ExactTables + the shared-memory image).
 template <int L>
 struct __align__(16) ExactArgs {
   // inner tables by position (class-major, sorted in the compare direction
   // inside a class), slot-major: tab[slot * 2^L + i]
   double tab[2 << L];
-  double gpre[2][n_groups(L)][kGroupSlots];  // group prefix sums per slot
-  // I15 screen (i15_on<L>()), per slot: the screened value k of every
-  // position in both 16-bit lanes (k | k << 16), the per-class map (scale,
-  // offset) and the class prefix sums P_c[n], n = 0..|c|, at
-  // cpre[slot][class_start(L, c) + c + n]
-  __align__(16) unsigned xq[2][i15_on<L>() ? (1 << L) : 4];
-  // end (exclusive, class-relative) of the tie run starting at each
-  // position: the following positions whose value is within 2^-44 relative
-  // of it (a leaf whose value ties with the threshold's to that precision
-  // contributes ~0 either way, so a tie run is classified as one leaf)
-  unsigned char te[2][i15_on<L>() ? (1 << L) : 4];
-  double cpre[2][i15_on<L>() ? (1 << L) + L + 1 : 1];
-  float nrm_s[2][L + 1], nrm_o[2][L + 1];
   double mid_c[kMidMax], mid_e[kMidMax], mid_mx[kMidMax], mid_mn[kMidMax];
   int mid_h[kMidMax];
   double w[kMaxN + 2];    // e^{-qT} p^h (1-p)^{N-h}, h = 0..N (zero padded)
   double e_cls[L + 1];    // S_N / S_node for an inner suffix with c ups
   double b_cls[L + 1];    // leaves per class, C(L, c)
+  // I15 screen: per slot and class, the monotone map (scale, offset)
+  float nrm_s[2][L + 1], nrm_o[2][L + 1];
   ExactScalars s;
 };
+
+// Host-side tables of a K1 argument block (built with it): the group prefix
+// sums of the Gray tables and, for the I15 screen, per slot the screened
+// value k of every position in both 16-bit lanes (k | k << 16), the end
+// (exclusive, class-relative) of the tie run starting at each position (the
+// following positions within 2^-44 relative: a leaf whose value ties with
+// the threshold's to that precision contributes the same either way, so a
+// tie run is classified as one leaf) and the class prefix sums P_c[n],
+// n = 0..|c|, at cpre[slot][class_start(L, c) + c + n].  cpre also travels
+// to the device after the shared-memory image (the exact walk reads it).
+template <int L>
+struct ExactTables {
+  double gpre[2][n_groups(L)][kGroupSlots];
+  unsigned xq[2][1 << L];
+  unsigned char te[2][1 << L];
+  double cpre[2][(1 << L) + L + 1];
+};
+template <int L>
+__host__ __device__ constexpr size_t cpre_doubles() { return (size_t)2 * ((1 << L) + L + 1); }
 
 // Generic per-path walk (any per-step probabilities, any N, all kinds).
 struct GenericArgs {

@@ -7,12 +7,6 @@
 #include "bp_kernels.h"
 #include "bp_leaf.cuh"
 
-#if BP_FOLD && !BP_GRAY
-#error "BP_FOLD needs the Gray tables (BP_GRAY=1)"
-#endif
-#ifndef BP_TAB_SMEM
-#define BP_TAB_SMEM 0  // inner tables: 0 = constant bank (uniform LDCU), 1 = shared memory (LDS.128)
-#endif
 
 
 namespace bp {
@@ -66,25 +60,26 @@ k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_
   constexpr int NP = kNodesPerBlock;
 
   __shared__ unsigned long long shist[kMaxN + 2];
-#if BP_GRAY && BP_FOLD && !BP_TAB_SMEM
-  // The shared tables as ONE image (k1_smem_layout): the weights (zero
-  // padded), the lookback kinds' W1/W2, the Gray tables (I15: only the small
-  // classes' on the Asian slot 0), and the I15 entry tables, screened values
-  // and tie-run ends of slot 0.  The host builds the image once per lattice
-  // after the argument block (ga); every CTA copies it with 16-byte loads.
-  // The I15 screen runs on the Asian slot; the lookback thresholds are ratios
-  // of lattice prices that tie with the table values, so those kinds keep the
-  // fp64 block.
+  static_assert(BP_GRAY && BP_FOLD, "K1 runs the Gray-code fold leaf block");
+  // The shared tables as ONE image (k1_smem_layout, dynamic shared memory):
+  // the weights (zero padded), the lookback kinds' W1/W2, the Gray tables of
+  // the classes the screen leaves to fp64 compares, and per screened slot the
+  // I15 entry tables, screened values and tie-run ends.  The host builds the
+  // image once per lattice after the argument block (ga, device memory);
+  // every CTA copies it with 16-byte loads.  After the image come the class
+  // prefix sums the exact walk reads (global memory).
   constexpr K1SmemLayout LY = k1_smem_layout<L>(KM);
   constexpr bool I15 = LY.i15[0] || LY.i15[1];
   constexpr bool needW = LY.need_w;
   static_assert(kGraySlots == 64, "k1_smem_layout assumes 64 Gray slots per group");
-  __shared__ __align__(16) unsigned char simg[LY.total];
-  double* sw = reinterpret_cast<double*>(simg + LY.sw);
-  double* sW1 = reinterpret_cast<double*>(simg + LY.sW1);
-  double* sW2 = reinterpret_cast<double*>(simg + LY.sW2);
-  if (ga) {
-    const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(ga) + align16(sizeof(ExactArgs<L>)));
+  extern __shared__ __align__(16) unsigned char simg[];
+  const double* sw = reinterpret_cast<const double*>(simg + LY.sw);
+  const double* sW1 = reinterpret_cast<const double*>(simg + LY.sW1);
+  const double* sW2 = reinterpret_cast<const double*>(simg + LY.sW2);
+  const char* gimg = reinterpret_cast<const char*>(ga) + align16(sizeof(ExactArgs<L>));
+  const double* gcpre = reinterpret_cast<const double*>(gimg + LY.total);
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(gimg);
     uint4* dst = reinterpret_cast<uint4*>(simg);
     // every load of the thread issued before the first store (one memory latency)
     constexpr int n16 = (int)(LY.total / 16), per = (n16 + 255) / 256;
@@ -99,88 +94,8 @@ k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_
       const int i = threadIdx.x + 256 * r;
       if (i < n16) dst[i] = v[r];
     }
-  } else {
-    // no image: build the tables here from the parameter bank
-    for (int i = threadIdx.x; i < kMaxN + 2 + NC; i += blockDim.x) sw[i] = (i < kMaxN + 2) ? a.w[i] : 0.0;
-#pragma unroll
-    for (int t = 0; t < 2; ++t) {
-      if (t >= NT) break;
-      double2* g = reinterpret_cast<double2*>(simg + LY.sgray[t]);
-      if (LY.i15[t]) {
-        gray_fill_small<L, 0>(a.gpre[t], g);
-        if (t == 0)
-          i15_fill<L, 0>(ParamTabs<L, 0>{a}, reinterpret_cast<double2*>(simg + LY.si15[0]), LY.lookback[0]);
-        else
-          i15_fill<L, 0>(ParamTabs<L, 1>{a}, reinterpret_cast<double2*>(simg + LY.si15[1]), LY.lookback[1]);
-        for (int i = threadIdx.x; i < (1 << L); i += blockDim.x) {
-          reinterpret_cast<unsigned*>(simg + LY.sxq[t])[i] = a.xq[t][i];
-          simg[LY.ste[t] + i] = a.te[t][i];
-        }
-      } else {
-        for (int i = threadIdx.x; i < NG * kGraySlots; i += blockDim.x)
-          g[i] = gray_table_entry(&a.gpre[t][i / kGraySlots][0], (unsigned)(i % kGraySlots), true);
-      }
-    }
-    if constexpr (needW) {
-      __syncthreads();
-      // W1[h] = sum_c w[h+c] C(L,c), W2[h] = sum_c w[h+c] C(L,c) e_c (the lookback
-      // kinds' out-of-the-money and terminal terms), fixed order
-      for (int i = threadIdx.x; i < kMaxN + 2; i += blockDim.x) {
-        double w1 = 0.0, w2 = 0.0;
-        for (int c = 0; c < NC; ++c) {
-          w1 = fma(sw[i + c], a.b_cls[c], w1);
-          w2 = fma(sw[i + c] * a.b_cls[c], a.e_cls[c], w2);
-        }
-        sW1[i] = w1;
-        sW2[i] = w2;
-      }
-    }
   }
 #define BP_GTAB(SLOT) reinterpret_cast<const char*>(simg + LY.sgray[SLOT])
-#define BP_LEAF(SLOT, GTV, TH) leaf_block_gray<L, NP, SLOT, GTV>(tb, BP_GTAB(SLOT), TH, acc, cnt)
-#else
-  // diagnostic configurations (BP_GRAY=0, BP_FOLD=0, BP_TAB_SMEM=1): tables built here
-  constexpr bool I15 = false;
-  __shared__ double sw[kMaxN + 2 + NC];
-#if BP_GRAY
-  __shared__ __align__(16) double2 sgray0[NT > 0 ? NG * kGraySlots : 1];
-  __shared__ __align__(16) double2 sgray1[NT > 1 ? NG * kGraySlots : 1];
-  if constexpr (NT > 0)
-    for (int i = threadIdx.x; i < NG * kGraySlots; i += blockDim.x)
-      sgray0[i] = gray_table_entry(&a.gpre[0][i / kGraySlots][0], (unsigned)(i % kGraySlots), BP_FOLD != 0);
-  if constexpr (NT > 1)
-    for (int i = threadIdx.x; i < NG * kGraySlots; i += blockDim.x)
-      sgray1[i] = gray_table_entry(&a.gpre[1][i / kGraySlots][0], (unsigned)(i % kGraySlots), BP_FOLD != 0);
-#define BP_GTAB(SLOT) reinterpret_cast<const char*>((SLOT) == 0 ? &sgray0[0] : &sgray1[0])
-#define BP_LEAF(SLOT, GTV, TH) leaf_block_gray<L, NP, SLOT, GTV>(tb, BP_GTAB(SLOT), TH, acc, cnt)
-#else
-  __shared__ double sgpre[NT > 0 ? NT : 1][NG * kGroupSlots];
-  for (int t = 0; t < NT; ++t)
-    for (int i = threadIdx.x; i < NG * kGroupSlots; i += blockDim.x) sgpre[t][i] = (&a.gpre[t][0][0])[i];
-#define BP_LEAF(SLOT, GTV, TH) leaf_block<L, NP, SLOT, GTV>(tb, sgpre[SLOT], TH, acc, cnt)
-#endif
-#if BP_TAB_SMEM
-  __shared__ __align__(16) double stab[NT > 0 ? NT << L : 2];
-  for (int i = threadIdx.x; i < (NT << L); i += blockDim.x) stab[i] = a.tab[i];
-#endif
-  for (int i = threadIdx.x; i < kMaxN + 2 + NC; i += blockDim.x) sw[i] = (i < kMaxN + 2) ? a.w[i] : 0.0;
-#if BP_FOLD
-  constexpr bool needW = kFL_ || kFLP_;
-  __shared__ double sW1[needW ? kMaxN + 2 : 1], sW2[needW ? kMaxN + 2 : 1];
-  if (needW) {
-    __syncthreads();
-    for (int i = threadIdx.x; i < kMaxN + 2; i += blockDim.x) {
-      double w1 = 0.0, w2 = 0.0;
-      for (int c = 0; c < NC; ++c) {
-        w1 = fma(sw[i + c], a.b_cls[c], w1);
-        w2 = fma(sw[i + c] * a.b_cls[c], a.e_cls[c], w2);
-      }
-      sW1[i] = w1;
-      sW2[i] = w2;
-    }
-  }
-#endif
-#endif
   if (CNT)
     for (int i = threadIdx.x; i < kMaxN + 2; i += blockDim.x) shist[i] = 0ull;
   __syncthreads();
@@ -233,21 +148,17 @@ k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_
         thN[p] = kFLP_ ? fmin(Mnn[p], sc.K) * rS : 0.0;
       }
 
-#if BP_TAB_SMEM
-      const double2* tb = reinterpret_cast<const double2*>(stab) + zoff;  // + 0, opaque
-#else
       const double2* tb = reinterpret_cast<const double2*>(a.tab) + zoff;  // + 0, opaque
-#endif
       // --- per kind: the leaf block (2^L explicit leaf tests per node), then
       // the class finalisation, node value = sum_c w[h+c] * contrib_c.  Kinds
       // run one after the other so only one kind's accumulators are live.
-#if BP_FOLD
       // the leaf block of a slot: the I15 screen where the layout puts it (the
       // lookback slots fix every lane's boundary leaf without a branch)
 #define BP_FOLDLEAF(SLOT, GTV, TH)                                                                            \
   if constexpr (LY.i15[SLOT])                                                                                \
     leaf_block_fold_i15<L, SLOT, GTV, LY.lookback[SLOT]>(                                                    \
-        ParamTabs<L, SLOT>{a}, reinterpret_cast<const uint4*>(simg + LY.sxq[SLOT]) + zoff,                   \
+        ParamTabs<L, SLOT>{a, gcpre + (SLOT) * ((1 << L) + L + 1)},                                          \
+        reinterpret_cast<const uint4*>(simg + LY.sxq[SLOT]) + zoff,                                          \
         I15Ctx{reinterpret_cast<const char*>(simg + LY.si15[SLOT]),                                          \
                reinterpret_cast<const unsigned*>(simg + LY.sxq[SLOT]), simg + LY.ste[SLOT],                 \
                1u | (unsigned)sc.zero, {0.f, 0.f}},                                                          \
@@ -288,70 +199,6 @@ k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_
           comp_add(ts[kFLP], tc[kFLP], fma(flat, sW1[hn[p]] - sN[p], fma(sc.K, sN[p], -Sn[p] * sA[p])));
         }
       }
-#else
-      if (kAC_) {
-        double acc[NP][NC];
-        int cnt[NP][NC];
-        zero_acc<NP, NC>(acc, cnt);
-        BP_LEAF(slotAC, true, thC);
-#pragma unroll
-        for (int p = 0; p < NP; ++p) {
-          double v = 0.0;
-#pragma unroll
-          for (int c = 0; c < NC; ++c) v = fma(sw[hn[p] + c], fma(Sn[p], acc[p][c], base[p] * (double)cnt[p][c]), v);
-          comp_add(ts[kAC], tc[kAC], v);
-        }
-      }
-      if (kAP_) {
-        double acc[NP][NC];
-        int cnt[NP][NC];
-        zero_acc<NP, NC>(acc, cnt);
-        BP_LEAF(slotAP, false, thC);
-#pragma unroll
-        for (int p = 0; p < NP; ++p) {
-          double v = 0.0;
-#pragma unroll
-          for (int c = 0; c < NC; ++c) v = fma(sw[hn[p] + c], fma(-Sn[p], acc[p][c], -base[p] * (double)cnt[p][c]), v);
-          comp_add(ts[kAP], tc[kAP], v);
-        }
-      }
-      if constexpr (kFL_) {
-        double acc[NP][NC];
-        int cnt[NP][NC];
-        zero_acc<NP, NC>(acc, cnt);
-        BP_LEAF(slotFL, true, thX);
-#pragma unroll
-        for (int p = 0; p < NP; ++p) {
-          double v = 0.0;
-#pragma unroll
-          for (int c = 0; c < NC; ++c) {
-            // S A + Mx (C_c - n) - S e_c C_c
-            const double bc = a.b_cls[c];
-            const double t = fma(Sn[p], acc[p][c], Mxn[p] * (bc - (double)cnt[p][c]));
-            v = fma(sw[hn[p] + c], fma(-Sn[p] * a.e_cls[c], bc, t), v);
-          }
-          comp_add(ts[kFL], tc[kFL], v);
-        }
-      }
-      if constexpr (kFLP_) {
-        double acc[NP][NC];
-        int cnt[NP][NC];
-        zero_acc<NP, NC>(acc, cnt);
-        BP_LEAF(slotFLP, false, thN);
-#pragma unroll
-        for (int p = 0; p < NP; ++p) {
-          double v = 0.0;
-          const double flat = fmax(sc.K - Mnn[p], 0.0);
-#pragma unroll
-          for (int c = 0; c < NC; ++c) {
-            const double n = (double)cnt[p][c];
-            const double t = fma(sc.K, n, -Sn[p] * acc[p][c]);
-            v = fma(sw[hn[p] + c], fma(a.b_cls[c] - n, flat, t), v);
-          }
-          comp_add(ts[kFLP], tc[kFLP], v);
-        }
-      }
-#endif
       if (kEC_ || kEP_) {
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
@@ -399,9 +246,22 @@ k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_
   }
 }
 
-#undef BP_LEAF
 #undef BP_GTAB
 #undef BP_FOLDLEAF
+
+// the dynamic shared-memory size of both instantiations (once per process
+// and device; beyond 48 KB it must be opted into)
+template <int L, unsigned KM>
+void fast_smem_attr() {
+  static bool done[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || done[dev]) return;
+  constexpr int smem = (int)k1_smem_layout<L>(KM).total;
+  cudaFuncSetAttribute(k_exact_fast<L, KM, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_exact_fast<L, KM, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  done[dev] = true;
+}
 
 // launch wrappers
 template <int L, unsigned KM>
@@ -409,20 +269,25 @@ cudaError_t launch_fast_t(const void* args, bool cnt, int grid, cudaStream_t st,
                           unsigned long long* hist, const void* dev_args) {
   const ExactArgs<L>& a = *static_cast<const ExactArgs<L>*>(args);
   const ExactArgs<L>* ga = static_cast<const ExactArgs<L>*>(dev_args);
+  if (!ga) return cudaErrorInvalidValue;  // K1 needs its device image
+  constexpr size_t smem = k1_smem_layout<L>(KM).total;
+  fast_smem_attr<L, KM>();
   if (cnt)
-    k_exact_fast<L, KM, true><<<grid, 256, 0, st>>>(a, unit_out, hist, ga);
+    k_exact_fast<L, KM, true><<<grid, 256, smem, st>>>(a, unit_out, hist, ga);
   else
-    k_exact_fast<L, KM, false><<<grid, 256, 0, st>>>(a, unit_out, hist, ga);
+    k_exact_fast<L, KM, false><<<grid, 256, smem, st>>>(a, unit_out, hist, ga);
   return cudaGetLastError();
 }
 
 template <int L, unsigned KM>
 int occupancy_fast_t(bool cnt) {
   int n = 0;
+  constexpr size_t smem = k1_smem_layout<L>(KM).total;
+  fast_smem_attr<L, KM>();
   if (cnt)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_exact_fast<L, KM, true>, 256, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_exact_fast<L, KM, true>, 256, smem);
   else
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_exact_fast<L, KM, false>, 256, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_exact_fast<L, KM, false>, 256, smem);
   return n;
 }
 

@@ -266,12 +266,11 @@ __host__ __device__ constexpr int ctz_c(int v) {
 template <int L, int SLOT>
 struct ParamTabs {
   const ExactArgs<L>& a;
+  const double* cp;  // the slot's class prefix sums (device image, global memory)
   __host__ __device__ __forceinline__ float nrm_s(int c) const { return a.nrm_s[SLOT][c]; }
   __host__ __device__ __forceinline__ float nrm_o(int c) const { return a.nrm_o[SLOT][c]; }
   __host__ __device__ __forceinline__ double tab(int i) const { return a.tab[SLOT * (1 << L) + i]; }
-  __host__ __device__ __forceinline__ double cpre(int i) const { return a.cpre[SLOT][i]; }
-  __host__ __device__ __forceinline__ unsigned xq(int i) const { return a.xq[SLOT][i]; }
-  __host__ __device__ __forceinline__ unsigned te(int i) const { return a.te[SLOT][i]; }
+  __host__ __device__ __forceinline__ double cpre(int i) const { return cp[i]; }
 };
 struct SmemTabs {
   const float *ns, *no;
