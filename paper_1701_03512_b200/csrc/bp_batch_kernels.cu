@@ -18,7 +18,7 @@
 
 namespace bp {
 
-constexpr int kBL = 8;   // inner bits
+constexpr int kBL = 9;   // inner bits (as K1; the screen's per-class work amortizes over bigger classes)
 constexpr int kBM = 6;   // middle bits
 constexpr int kBThreads = 256;
 constexpr int kBNP = 2;  // nodes per leaf block
@@ -28,6 +28,31 @@ struct BatchArgs {
   unsigned kind;
   BatchLayout lay;
 };
+
+// group prefix sums of class C (compile-time layout: no runtime binomials)
+template <int C, bool SMALL_ONLY>
+__device__ inline void batch_group_prefix(const double* __restrict__ tab, double* __restrict__ gpre) {
+  if constexpr (C <= kBL) {
+    if constexpr (!(SMALL_ONLY && i15_class(kBL, C))) {
+      constexpr int ng = class_groups(kBL, C), g0 = group_base(kBL, C), size = binom(kBL, C);
+      for (int gi = threadIdx.x; gi < ng * kGroupSlots; gi += blockDim.x) {
+        const int gl = gi / kGroupSlots, n = gi % kGroupSlots;
+        const int len = min(kGroup, size - kGroup * gl);
+        const int i0 = class_start(kBL, C) + kGroup * gl;
+        double s = 0.0, cc = 0.0;
+        for (int k = 0; k < n && k < len; ++k) comp_add(s, cc, tab[i0 + k]);
+        gpre[g0 * kGroupSlots + gi] = s + cc;
+      }
+    }
+    batch_group_prefix<C + 1, SMALL_ONLY>(tab, gpre);
+  }
+}
+
+// next integer with the same number of set bits (Gosper's hack)
+__device__ __forceinline__ int next_same_popc(int v) {
+  const int c = v & -v, r = v + c;
+  return (((r ^ v) >> 2) / c) | r;
+}
 
 template <unsigned KIND>
 #ifndef BP_K3_MINB
@@ -57,7 +82,7 @@ k_exact_batch(const BatchOption* __restrict__ opts, BatchArgs ba, double2* __res
   __shared__ int mid_h[NMID];
   __shared__ double w[kMaxN + 2 + NC];
   __shared__ double e_cls[NC], b_cls[NC];
-  __shared__ double red_s[kBThreads], red_c[kBThreads];
+  __shared__ double red_s[kBThreads / 32], red_c[kBThreads / 32];
 
   // CTA -> (option, part of 2^parts_log2): whole-layout options first, then the split tail
   const long long head = (long long)ba.lay.n_whole << ba.lay.base_log2;
@@ -72,32 +97,45 @@ k_exact_batch(const BatchOption* __restrict__ opts, BatchArgs ba, double2* __res
 
   // ---- inner table: value of leaf s, then its position (class-major, sorted
   // in the compare direction inside the class; ties by leaf index)
-  double v = 0.0;
-  if (TAB && tid < NL) {
-    double r = 1.0, c = 0.0, mx = 0.0, mn = INFINITY;
-    for (int j = 0; j < kBL; ++j) {
-      r *= ((tid >> (kBL - 1 - j)) & 1) ? o.u : o.d;
-      c += r;
-      mx = fmax(mx, r);
-      mn = fmin(mn, r);
+  constexpr int PER = (NL + kBThreads - 1) / kBThreads;  // positions per thread
+  double v[PER];
+  int pos[PER];
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int sfx = tid + kBThreads * q;
+    v[q] = 0.0;
+    pos[q] = -1;
+    if (TAB && sfx < NL) {
+      double r = 1.0, c = 0.0, mx = 0.0, mn = INFINITY;
+      for (int j = 0; j < kBL; ++j) {
+        r *= ((sfx >> (kBL - 1 - j)) & 1) ? o.u : o.d;
+        c += r;
+        mx = fmax(mx, r);
+        mn = fmin(mn, r);
+      }
+      v[q] = (AC || AP) ? c : FL ? mx : mn;
+      tab[sfx] = v[q];
     }
-    v = (AC || AP) ? c : FL ? mx : mn;
-    tab[tid] = v;
   }
   __syncthreads();
-  int pos = -1;
-  if (TAB && tid < NL) {
-    const int cls = __popc(tid);
-    int rank = 0;
-    for (int s2 = 0; s2 < NL; ++s2) {
-      if (__popc(s2) != cls) continue;
-      const double v2 = tab[s2];
-      rank += DESC ? (v2 > v || (v2 == v && s2 < tid)) : (v2 < v || (v2 == v && s2 < tid));
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int sfx = tid + kBThreads * q;
+    if (TAB && sfx < NL) {
+      const int cls = __popc(sfx);
+      int rank = 0;
+      // the class's leaves only: every cls-bit pattern below 2^kBL in order
+      for (int s2 = (1 << cls) - 1; s2 < NL; s2 = cls ? next_same_popc(s2) : NL) {
+        const double v2 = tab[s2];
+        rank += DESC ? (v2 > v[q] || (v2 == v[q] && s2 < sfx)) : (v2 < v[q] || (v2 == v[q] && s2 < sfx));
+      }
+      pos[q] = class_start(kBL, cls) + rank;
     }
-    pos = class_start(kBL, cls) + rank;
   }
   __syncthreads();
-  if (pos >= 0) tab[pos] = v;
+#pragma unroll
+  for (int q = 0; q < PER; ++q)
+    if (pos[q] >= 0) tab[pos[q]] = v[q];
   for (int j = tid; j < NMID; j += kBThreads) {
     double r = 1.0, c = 0.0, mx = 0.0, mn = INFINITY;
     int h = 0;
@@ -124,19 +162,9 @@ k_exact_batch(const BatchOption* __restrict__ opts, BatchArgs ba, double2* __res
     b_cls[tid] = (double)binom(kBL, tid);
   }
   __syncthreads();
-  // group prefix sums (compensated, rounded once), one (group, n) per thread
-  if (TAB)
-    for (int gi = tid; gi < NG * kGroupSlots; gi += kBThreads) {
-      const int g = gi / kGroupSlots, n = gi % kGroupSlots;
-      int cls = 0;
-      while (cls < kBL && group_base(kBL, cls + 1) <= g) ++cls;
-      const int gl = g - group_base(kBL, cls);
-      const int len = min(kGroup, binom(kBL, cls) - kGroup * gl);
-      const int i0 = class_start(kBL, cls) + kGroup * gl;
-      double s = 0.0, cc = 0.0;
-      for (int k = 0; k < n && k < len; ++k) comp_add(s, cc, tab[i0 + k]);
-      gpre[gi] = s + cc;
-    }
+  // group prefix sums (compensated, rounded once), one (group, n) per thread;
+  // the screened kinds need only the small classes' groups
+  if (TAB) batch_group_prefix<0, I15>(tab, gpre);
   // lookback kinds: per node up count h, W1[h] = sum_c w[h+c] C(L,c) and
   // W2[h] = sum_c w[h+c] C(L,c) e_c (out-of-the-money and terminal terms)
   if (FL || FLP)
@@ -179,17 +207,17 @@ k_exact_batch(const BatchOption* __restrict__ opts, BatchArgs ba, double2* __res
     }
     __syncthreads();
     // per position: the screened value in both lanes and the tie-run end
-    if (tid < NL) {
+    for (int i = tid; i < NL; i += kBThreads) {
       int c = 0;
-      while (tid >= class_start(kBL, c + 1)) ++c;
+      while (i >= class_start(kBL, c + 1)) ++c;
       if (i15_class(kBL, c)) {
         const int i0 = class_start(kBL, c), len = binom(kBL, c);
-        const unsigned k = i15_map((float)tab[tid], i15_s[c], i15_o[c]);
-        i15_xq[tid] = k | (k << 16);
-        const double tol = ldexp(fabs(tab[tid]), -44);
-        int e = tid - i0 + 1;
-        while (e < len && fabs(tab[i0 + e] - tab[tid]) <= tol) ++e;
-        i15_te[tid] = (unsigned char)e;
+        const unsigned k = i15_map((float)tab[i], i15_s[c], i15_o[c]);
+        i15_xq[i] = k | (k << 16);
+        const double tol = ldexp(fabs(tab[i]), -44);
+        int e = i - i0 + 1;
+        while (e < len && fabs(tab[i0 + e] - tab[i]) <= tol) ++e;
+        i15_te[i] = (unsigned char)e;
       }
     }
     __syncthreads();
@@ -271,22 +299,20 @@ k_exact_batch(const BatchOption* __restrict__ opts, BatchArgs ba, double2* __res
       }
     }
   }
-  // fixed-order CTA reduce
-  red_s[tid] = ts;
-  red_c[tid] = tc;
-  __syncthreads();
-  for (int stride = kBThreads / 2; stride > 0; stride >>= 1) {
-    if (tid < stride) {
-      double a = red_s[tid], c = red_c[tid];
-      comp_merge(a, c, red_s[tid + stride], red_c[tid + stride]);
-      red_s[tid] = a;
-      red_c[tid] = c;
-    }
-    __syncthreads();
+  // fixed-order CTA reduce: warp shuffle trees, then warp 0 over the 8 warp sums
+  warp_comp_reduce(ts, tc);
+  if ((tid & 31) == 0) {
+    red_s[tid >> 5] = ts;
+    red_c[tid >> 5] = tc;
   }
-  if (tid == 0) {
-    const double f = (AC || AP) ? 1.0 / N : 1.0;
-    partial[blockIdx.x] = make_double2(red_s[0] * f, red_c[0] * f);
+  __syncthreads();
+  if (tid < 32) {
+    double a = tid < kBThreads / 32 ? red_s[tid] : 0.0, c = tid < kBThreads / 32 ? red_c[tid] : 0.0;
+    warp_comp_reduce(a, c);
+    if (tid == 0) {
+      const double f = (AC || AP) ? 1.0 / N : 1.0;
+      partial[blockIdx.x] = make_double2(a * f, c * f);
+    }
   }
 }
 
@@ -311,7 +337,7 @@ BatchLayout batch_layout(int n_opts, int N) {
     const char* e = std::getenv("BINPATHS_BATCH_CPO_LOG2");  // diagnostics: uniform CTAs per option
     return e ? std::atoi(e) : -1;
   }();
-  const int max_log2 = std::min(4, N - 14);  // >= 1 thread prefix per CTA
+  const int max_log2 = std::min(4, N - kBL - kBM);  // >= 1 thread prefix per CTA
   int dev = 0, sms = 148, occ = 3;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
