@@ -30,7 +30,7 @@ __host__ __device__ constexpr int fast_tables(unsigned km) {
   return (int)((km >> kAC) & 1) + (int)((km >> kAP) & 1) + (int)((km >> kFL) & 1) + (int)((km >> kFLP) & 1);
 }
 #ifndef BP_MINB1
-#define BP_MINB1 3  // resident CTAs per SM targeted by the one-table kernels
+#define BP_MINB1 2  // resident CTAs per SM targeted by the one-table kernels (r2 scan at L = 9: 2 beats 3)
 #endif
 #ifndef BP_MINB2
 #define BP_MINB2 2  // ... and by the fused two-table kernels
