@@ -212,8 +212,15 @@ static Layout choose_layout(const bp_tree* t, uint32_t payoffs, uint32_t flags, 
       const char* e = std::getenv("BINPATHS_UNIT_LOG2");
       return e ? std::atoi(e) : kUnitTargetLog2;
     }();
-    // n_mid = 2^m is a multiple of the nodes per leaf block
-    lay.m = std::max(std::max(1, kNodesPerBlockLog2), std::min(6, free_bits - target));
+    // n_mid = 2^m is a multiple of the nodes per leaf block; at most 2^kMidCap
+    // nodes per lane per unit keeps >= ~14 units per warp at 8 ranks for the
+    // N = 36 tree (wave quantization), at ~1 % more prefix walks
+    static const int mid_cap = [] {
+      const char* e = std::getenv("BINPATHS_MID_CAP");  // diagnostics
+      const int v = e ? std::atoi(e) : kMidCap;
+      return (v >= 1 && v <= 6) ? v : kMidCap;
+    }();
+    lay.m = std::max(std::max(1, kNodesPerBlockLog2), std::min(mid_cap, free_bits - target));
     lay.Dp = lay.D - lay.m;
     const int unit_bits = free_bits - lay.m;
     lay.q = std::max(0, unit_bits - 18);
