@@ -96,6 +96,18 @@ k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_
     }
   }
 #define BP_GTAB(SLOT) reinterpret_cast<const char*>(simg + LY.sgray[SLOT])
+  // nibble tables of the prefix walk: 4 steps with up pattern nb (first step = bit 3)
+  __shared__ double4 snib[16];
+  if (threadIdx.x < 16) {
+    double r = 1.0, c = 0.0, mx = 0.0, mn = __longlong_as_double(0x7ff0000000000000ll);
+    for (int l = 0; l < 4; ++l) {
+      r *= ((threadIdx.x >> (3 - l)) & 1) ? a.s.u : a.s.d;
+      c += r;
+      mx = fmax(mx, r);
+      mn = fmin(mn, r);
+    }
+    snib[threadIdx.x] = make_double4(r, c, mx, mn);
+  }
   if (CNT)
     for (int i = threadIdx.x; i < kMaxN + 2; i += blockDim.x) shist[i] = 0ull;
   __syncthreads();
@@ -113,16 +125,29 @@ k_exact_fast(const __grid_constant__ ExactArgs<L> a, double2* __restrict__ unit_
     for (int k = 0; k < kNumKinds; ++k) { ts[k] = 0.0; tc[k] = 0.0; }
    for (unsigned long long rr = 0; rr < (1ull << sc.q); ++rr) {
     const unsigned long long tp = (((unit << sc.q) | rr) << 5) | (unsigned long long)lane;  // thread prefix, Dp bits
-    // --- prefix walk: steps 1..Dp (reference asset_path, model.py:164-172)
+    // --- prefix walk: steps 1..Dp (reference asset_path, model.py:164-172):
+    // the first Dp mod 4 steps one by one, then four steps per nibble-table
+    // lookup (relative price after the nibble, sum, max and min of its
+    // relative prices)
     double S = sc.S0, Sig = 0.0, Mx = 0.0, Mn = INF;
     int h = 0;
-    for (int t = sc.Dp - 1; t >= 0; --t) {
+    int t = sc.Dp - 1;
+    for (; t >= 0 && ((t + 1) & 3); --t) {
       const int b = (int)((tp >> t) & 1ull);
       S *= b ? sc.u : sc.d;
       Sig += S;
       if (needMx) Mx = fmax(Mx, S);
       if (needMn) Mn = fmin(Mn, S);
       h += b;
+    }
+    for (; t >= 3; t -= 4) {
+      const int nb = (int)((tp >> (t - 3)) & 15ull);
+      const double4 q = snib[nb];  // {e, c, mx, mn}
+      Sig = fma(S, q.y, Sig);
+      if (needMx) Mx = fmax(Mx, S * q.z);
+      if (needMn) Mn = fmin(Mn, S * q.w);
+      S *= q.x;
+      h += __popc(nb);
     }
 
     // nodes are processed NP at a time (n_mid is a multiple of NP: m >= 1)
