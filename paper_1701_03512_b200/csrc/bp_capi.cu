@@ -210,7 +210,7 @@ static Layout choose_layout(const bp_tree* t, uint32_t payoffs, uint32_t flags, 
     const int free_bits = lay.D - 5;  // bits above the lane
     static const int target = [] {
       const char* e = std::getenv("BINPATHS_UNIT_LOG2");
-      return e ? std::atoi(e) : kUnitTargetLog2;
+      return e ? std::atoi(e) : kFastUnitTargetLog2;
     }();
     // n_mid = 2^m is a multiple of the nodes per leaf block; at most 2^kMidCap
     // nodes per lane per unit keeps >= ~14 units per warp at 8 ranks for the
@@ -715,6 +715,19 @@ static int device_sm_count(int dev) {
 
 // Enqueue the valuation of super-blocks [sb_first, sb_first+sb_count) on
 // the current device.  out_dev: [sb_count][6][2] doubles (device).
+// Unit scratch of a valuation: a head of kScratchHead double2 (slot 0 = K1's
+// unit counter, 0 between launches: zeroed at allocation, reset by the K2
+// after every K1), then the unit partials [unit][kind].
+constexpr size_t kScratchHead = 16;
+static size_t scratch_need(unsigned long long n_units) {
+  return sizeof(double2) * (kScratchHead + (size_t)kNumKinds * n_units);
+}
+static cudaError_t scratch_alloc(double2** p, size_t bytes, cudaStream_t st) {
+  cudaError_t e = cudaMallocAsync((void**)p, bytes, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(*p, 0, sizeof(double2) * kScratchHead, st);
+  return e;
+}
+
 // ---------------------------------------------------------------------------
 // A prepared valuation: layout, prebuilt kernel arguments per kind group and
 // per-device scratch.  Building the tables costs host time (sorting, pow);
@@ -893,18 +906,20 @@ static int plan_enqueue(bp_exact_plan* P, int dev, int sb_first, int sb_count, d
   const unsigned long long u1 = u0 + (unsigned long long)sb_count * lay.units_per_sb;
   const unsigned long long n_units = u1 - u0;
   double2* unit_out = nullptr;
+  unsigned long long* work = nullptr;
   {
     std::lock_guard<std::mutex> g(P->mu);
     auto& sc = P->scratch[dev];
-    const size_t need = sizeof(double2) * kNumKinds * n_units;
+    const size_t need = scratch_need(n_units);
     if (sc.bytes < need) {
       if (sc.p) cudaFreeAsync(sc.p, st);
       sc.p = nullptr;
       sc.bytes = 0;
-      BP_CUDA(cudaMallocAsync((void**)&sc.p, need, st));
+      BP_CUDA(scratch_alloc(&sc.p, need, st));
       sc.bytes = need;
     }
-    unit_out = sc.p;
+    work = reinterpret_cast<unsigned long long*>(sc.p);
+    unit_out = sc.p + kScratchHead;
   }
   // kernels index unit_out by absolute unit; shift the base pointer
   double2* unit_base = unit_out - (ptrdiff_t)(u0 * kNumKinds);
@@ -960,13 +975,13 @@ static int plan_enqueue(bp_exact_plan* P, int dev, int sb_first, int sb_count, d
       const int occ = std::max(1, cached_occupancy_fast(lay.L, g.km, cnt_g));
       const int grid = (int)std::max<unsigned long long>(1, std::min<unsigned long long>(want, (unsigned long long)occ * sms));
       const auto tl0 = std::chrono::steady_clock::now();
-      BP_CUDA(launch_exact_fast(lay.L, g.km, g.args.data(), cnt_g, grid, st, unit_base, hist_dev, g.dargs[dev]));
+      BP_CUDA(launch_exact_fast(lay.L, g.km, g.args.data(), cnt_g, grid, st, unit_base, hist_dev, g.dargs[dev], work));
       const auto tl1 = std::chrono::steady_clock::now();
       if (trace_on())
         std::fprintf(stderr, "[bp trace] K1 launch %.1f us (%zu B of arguments)\n",
                      std::chrono::duration<double, std::micro>(tl1 - tl0).count(), g.args.size());
       BP_CUDA(launch_sb_reduce(unit_base, lay.units_per_sb, sb_first, sb_count, g.km, std::exchange(zero_kinds, 0u), 1.0 / P->tree.n_steps,
-                               out_dev, st));
+                               out_dev, st, work));
     }
   } else {
     GenericArgs g = P->gen;
@@ -1098,7 +1113,7 @@ static bool plan_enqueue_graph(bp_exact_plan* P, int dev, int sb_first, int sb_c
   {
     std::lock_guard<std::mutex> g(P->mu);
     scratch = P->scratch[dev].p;
-    const size_t need = sizeof(double2) * kNumKinds * (unsigned long long)sb_count * P->lay.units_per_sb;
+    const size_t need = scratch_need((unsigned long long)sb_count * P->lay.units_per_sb);
     if (!scratch || P->scratch[dev].bytes < need) return false;  // not sized yet: ordinary path first
     const bp_exact_plan::Graph key{dev, sb_first, sb_count, out_dev, scratch, nullptr};
     for (auto it = P->graphs.begin(); it != P->graphs.end(); ++it)
@@ -1300,13 +1315,13 @@ static bool try_graph_job(DevCtx& c, bp_exact_plan& P, DeviceJob* job, uint32_t 
   if (!graphs_enabled() || cnt || P.lay.engine != 1) return false;
   const int dev = job->device;
   const unsigned long long n_units = (unsigned long long)job->sb_count * P.lay.units_per_sb;
-  const size_t need = sizeof(double2) * kNumKinds * n_units;
+  const size_t need = scratch_need(n_units);
   if (c.scratch_bytes < need) {  // size the scratch outside any capture; graphs on the old buffer go
     c.drop_graphs();
     if (c.scratch) cudaFreeAsync(c.scratch, c.st);
     c.scratch = nullptr;
     c.scratch_bytes = 0;
-    if (cudaMallocAsync((void**)&c.scratch, need, c.st) != cudaSuccess) return false;
+    if (scratch_alloc(&c.scratch, need, c.st) != cudaSuccess) return false;
     c.scratch_bytes = need;
   }
   for (auto& g : P.groups) cached_occupancy_fast(P.lay.L, g.km, false);  // no queries inside the capture

@@ -51,6 +51,9 @@ BP_HD constexpr int kind_table(int k) {
 
 constexpr int kMidMax = 64;          // 2^m, m <= 6
 constexpr int kUnitTargetLog2 = 14;  // units >= 2^14 when the tree allows it (r1 scan)
+// K1 (units handed out dynamically): units >= 2^13 when the tree allows it
+// (r2 scan, N = 30: 2^13 units of 8 nodes per lane beat 2^14 of 4 by 2-4 %)
+constexpr int kFastUnitTargetLog2 = 13;
 constexpr int kMidCap = 5;           // at most 2^kMidCap middle nodes per lane per unit (BINPATHS_MID_CAP; r2 scan)
 constexpr int kMaxSB = 64;           // canonical super-blocks (top 6 bits of the unit index)
 constexpr int kFastMinN = 16;        // smaller trees use the per-path walk

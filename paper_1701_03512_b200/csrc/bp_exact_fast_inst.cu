@@ -8,7 +8,7 @@ namespace bp {
 
 #define BP_INST(LL, KMV)                                                                              \
   template cudaError_t launch_fast_t<LL, KMV>(const void*, bool, int, cudaStream_t, double2*,        \
-                                              unsigned long long*, const void*);                    \
+                                              unsigned long long*, const void*, unsigned long long*); \
   template int occupancy_fast_t<LL, KMV>(bool);
 
 #if BP_FAST_PART == 0

@@ -85,7 +85,9 @@ k_exact_generic(const __grid_constant__ GenericArgs a, double2* __restrict__ uni
 // output entry is written exactly once per step.
 __global__ void __launch_bounds__(256)
 k_sb_reduce(const double2* __restrict__ unit_out, unsigned long long units_per_sb, int sb_first,
-            unsigned kinds, unsigned zero_kinds, double scale_asian, double* __restrict__ out) {
+            unsigned kinds, unsigned zero_kinds, double scale_asian, double* __restrict__ out,
+            unsigned long long* __restrict__ work) {
+  if (work && blockIdx.x == 0 && threadIdx.x == 0) *work = 0ull;  // the K1 before us is done with it
   __shared__ double ws[kNumKinds][8], wc[kNumKinds][8];
   const unsigned long long u0 = (unsigned long long)(sb_first + blockIdx.x) * units_per_sb;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -127,7 +129,7 @@ k_sb_reduce(const double2* __restrict__ unit_out, unsigned long long units_per_s
 // (L, kind mask) in bp_exact_fast_inst.cu (compiled once per BP_FAST_PART).
 template <int L, unsigned KM>
 cudaError_t launch_fast_t(const void* args, bool cnt, int grid, cudaStream_t st, double2* unit_out,
-                          unsigned long long* hist, const void* dev_args);
+                          unsigned long long* hist, const void* dev_args, unsigned long long* work);
 template <int L, unsigned KM>
 int occupancy_fast_t(bool cnt);
 
@@ -144,9 +146,10 @@ bool fast_kind_mask_supported(unsigned km) {
 }
 
 cudaError_t launch_exact_fast(int L, unsigned km, const void* args, bool cnt, int grid, cudaStream_t st,
-                              double2* unit_out, unsigned long long* hist, const void* dev_args) {
+                              double2* unit_out, unsigned long long* hist, const void* dev_args,
+                              unsigned long long* work) {
 #define BP_CASE(LL, KMV) \
-  if (L == LL && km == (KMV)) return launch_fast_t<LL, (KMV)>(args, cnt, grid, st, unit_out, hist, dev_args);
+  if (L == LL && km == (KMV)) return launch_fast_t<LL, (KMV)>(args, cnt, grid, st, unit_out, hist, dev_args, work);
   BP_FAST_KMS(BP_CASE, 8)
   BP_FAST_KMS(BP_CASE, 9)
 #undef BP_CASE
@@ -189,8 +192,9 @@ int occupancy_exact_generic(bool cnt) {
 }
 
 cudaError_t launch_sb_reduce(const double2* unit_out, unsigned long long units_per_sb, int sb_first, int sb_count,
-                             unsigned kinds, unsigned zero_kinds, double scale_asian, double* out, cudaStream_t st) {
-  k_sb_reduce<<<sb_count, 256, 0, st>>>(unit_out, units_per_sb, sb_first, kinds, zero_kinds, scale_asian, out);
+                             unsigned kinds, unsigned zero_kinds, double scale_asian, double* out, cudaStream_t st,
+                             unsigned long long* work) {
+  k_sb_reduce<<<sb_count, 256, 0, st>>>(unit_out, units_per_sb, sb_first, kinds, zero_kinds, scale_asian, out, work);
   return cudaGetLastError();
 }
 

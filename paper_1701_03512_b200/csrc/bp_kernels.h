@@ -9,9 +9,12 @@
 namespace bp {
 
 bool fast_kind_mask_supported(unsigned km);
-// dev_args: a device copy of the argument block's tables (CTA setup reads), or nullptr
+// dev_args: a device copy of the argument block's tables (CTA setup reads).
+// work: the unit counter of the launch (device, 0 on entry; the K2 launched
+// after it resets it)
 cudaError_t launch_exact_fast(int L, unsigned km, const void* args, bool cnt, int grid, cudaStream_t st,
-                              double2* unit_out, unsigned long long* hist, const void* dev_args);
+                              double2* unit_out, unsigned long long* hist, const void* dev_args,
+                              unsigned long long* work);
 int occupancy_exact_fast(int L, unsigned km, bool cnt);
 size_t exact_args_size(int L);
 
@@ -19,8 +22,10 @@ cudaError_t launch_exact_generic(const GenericArgs& a, bool cnt, int grid, cudaS
                                  unsigned long long* hist);
 int occupancy_exact_generic(bool cnt);
 
+// work: a K1 unit counter to reset to 0 (stream order: after that K1), or nullptr
 cudaError_t launch_sb_reduce(const double2* unit_out, unsigned long long units_per_sb, int sb_first, int sb_count,
-                             unsigned kinds, unsigned zero_kinds, double scale_asian, double* out, cudaStream_t st);
+                             unsigned kinds, unsigned zero_kinds, double scale_asian, double* out, cudaStream_t st,
+                             unsigned long long* work = nullptr);
 
 // Batched exact (one option per CTA group), see bp_batch_kernels.cu
 struct BatchOption {

@@ -87,7 +87,7 @@ def main():
         res["predicted_efficiency"][G]["kernel_only"] = t1 / (G * r["kernel_ms"])
         res["predicted_efficiency"][G]["step_world1_measured"] = res["ranks"][1]["step_world1_ms"] / (
             G * r["step_world1_ms"])
-    res["unit_log2"] = os.environ.get("BINPATHS_UNIT_LOG2", "default (14)")
+    res["unit_log2"] = os.environ.get("BINPATHS_UNIT_LOG2", "default (13)")
     print(json.dumps(res, indent=1))
     dist.destroy_process_group()
 

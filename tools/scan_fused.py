@@ -17,5 +17,5 @@ for N, sigma, r, T, K, ks in cases:
     res = [bp.value_exact(req, kinds=ks, devices=[0]) for _ in range(5 if N < 36 else 3)]
     best = min(x.kernel_ms for x in res)
     vals = " ".join(f"{k}={v:.15g}" for k, v in res[-1].values.items())
-    print(f"{tag} unit={os.environ.get('BINPATHS_UNIT_LOG2', '14')} N={N} kinds={len(ks)} ms={best:.4f} "
+    print(f"{tag} unit={os.environ.get('BINPATHS_UNIT_LOG2', '13')} N={N} kinds={len(ks)} ms={best:.4f} "
           f"paths/s={2**N / best * 1e3:.3e} {vals}", flush=True)
