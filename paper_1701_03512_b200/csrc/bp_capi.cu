@@ -1273,9 +1273,31 @@ static bool graphs_enabled() {
   return on;
 }
 
-// the timing events sit outside the graph (kernel_ms then also holds the
-// 768-byte result copy at the graph's end)
+// K2 of a captured valuation writes the super-block partials straight into
+// the context's pinned host buffer (device-visible under unified addressing:
+// 64 x 12 posted 8-byte stores over PCIe), so the graph has no copy node
+// (BINPATHS_MAPPED_OUT=0: K2 -> device buffer -> D2H copy node)
+static bool mapped_out() {
+  static const bool on = [] {
+    const char* e = std::getenv("BINPATHS_MAPPED_OUT");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
+// BINPATHS_GRAPH_EVENTS=1: the timing events are event-record nodes of the
+// graph itself (no host-side record before the launch); default: recorded by
+// the host around the launch
+static bool graph_events() {
+  static const bool on = [] {
+    const char* e = std::getenv("BINPATHS_GRAPH_EVENTS");
+    return e && std::atoi(e) != 0;
+  }();
+  return on;
+}
+
 static bool launch_graph(DevCtx& c, cudaGraphExec_t exec) {
+  if (graph_events()) return cudaGraphLaunch(exec, c.st) == cudaSuccess;
   cudaEventRecord(c.e0, c.st);
   const bool ok = cudaGraphLaunch(exec, c.st) == cudaSuccess;
   cudaEventRecord(c.e1, c.st);
@@ -1339,10 +1361,12 @@ static bool try_graph_job(DevCtx& c, bp_exact_plan& P, DeviceJob* job, uint32_t 
   if (cudaStreamBeginCapture(c.st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) return false;
   P.scratch[dev].p = c.scratch;
   P.scratch[dev].bytes = c.scratch_bytes;
-  int rc = plan_enqueue(&P, dev, job->sb_first, job->sb_count, c.out_dev, nullptr, c.st);
+  if (graph_events()) cudaEventRecordWithFlags(c.e0, c.st, cudaEventRecordExternal);
+  int rc = plan_enqueue(&P, dev, job->sb_first, job->sb_count, mapped_out() ? c.out_host : c.out_dev, nullptr, c.st);
   P.scratch[dev].p = nullptr;
   P.scratch[dev].bytes = 0;
-  cudaMemcpyAsync(c.out_host, c.out_dev, sizeof(double) * np, cudaMemcpyDeviceToHost, c.st);
+  if (!mapped_out()) cudaMemcpyAsync(c.out_host, c.out_dev, sizeof(double) * np, cudaMemcpyDeviceToHost, c.st);
+  if (graph_events()) cudaEventRecordWithFlags(c.e1, c.st, cudaEventRecordExternal);
   const cudaError_t ec = cudaStreamEndCapture(c.st, &graph);
   cudaGraphExec_t exec = nullptr;
   if (rc || ec != cudaSuccess || !graph || cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
