@@ -13,6 +13,7 @@ from .oracle import (  # noqa: F401
     exact,
     exact_range,
     lib,
+    mc_bits,
     mc_range,
     mc_shared,
     mc_strata,

@@ -51,6 +51,9 @@ def lib():
         L.orc_mc_strata.restype = i
         L.orc_mc_range.argtypes = [i, d, d, d, d, pd, i, i, pu64, pu64, u64, ctypes.c_uint32, ctypes.c_uint32, pd, pd]
         L.orc_mc_range.restype = i
+        L.orc_mc_bits.argtypes = [i, i, pd, u64, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32,
+                                  ctypes.POINTER(ctypes.c_int)]
+        L.orc_mc_bits.restype = None
         L.orc_mc_shared.argtypes = [i, d, d, d, d, pd, i, i, u64, pd, u64, ctypes.c_uint32, ctypes.c_uint32,
                                     pd, pd, pd]
         L.orc_mc_shared.restype = i
@@ -113,6 +116,14 @@ def mc_strata(N, S0, K, u, d, probs, kind, r, draws, seed, rep0=0, n_reps=1):
                         draws.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), seed, rep0, n_reps,
                         _dp(theta), _dp(sse))
     return theta.reshape(n_reps, M), sse.reshape(n_reps, M)
+
+
+def mc_bits(N, r, probs, seed, stream=0, rep=0, draw=0):
+    """Up/down bits of the N - r suffix steps of one draw (the sampler alone)."""
+    probs = _probs(N, probs)
+    up = (ctypes.c_int * max(N - r, 1))()
+    lib().orc_mc_bits(N, r, _dp(probs), seed, stream, rep, draw, up)
+    return np.array(list(up)[:N - r], dtype=bool)
 
 
 def mc_range(N, S0, K, u, d, probs, kind, r, first, end, seed, rep0=0, n_reps=1):

@@ -1625,6 +1625,18 @@ static void fill_mc_args(const bp_tree* t, unsigned kind, int r, uint64_t seed, 
     }
     a.thr[i] = thr;
   }
+  // the sampler's bit planes: suffix step w = i - r sits at bit w % 32 of group w / 32
+  for (int i = r; i < t->n_steps; ++i) {
+    const int w = i - r, g = w >> 5;
+    const uint32_t bit = 1u << (w & 31);
+    if ((a.always[i / 32] >> (i % 32)) & 1u) {
+      a.forced[g] |= bit;
+      continue;
+    }
+    a.open[g] |= bit;
+    for (int l = 0; l < kMcLevels; ++l)
+      if ((a.thr[i] >> (31 - l)) & 1u) a.tmask[g][l] |= bit;
+  }
 }
 
 template <typename T>

@@ -45,10 +45,15 @@ cudaError_t launch_exact_batch(const BatchOption* opts_dev, const BatchLayout& l
                                double* values_dev, double2* scratch_dev, cudaStream_t st);
 
 // Monte Carlo, see bp_mc_kernels.cu
+constexpr int kMcLevels = 8;  // threshold bits compared bit-sliced before the tie words
 struct McArgs {
   double S0, K, u, d, invN;
   uint32_t thr[kMaxN];   // Bernoulli thresholds floor(p_t 2^32) (saturated)
   uint32_t always[2];    // bit t set: step t is always up (p_t >= 1)
+  // bit-sliced sampler (bp_mc_kernels.cu): suffix step w = 32 g + b is bit b of group g
+  uint32_t tmask[2][kMcLevels];  // level i: bit b = bit (31 - i) of the step's threshold
+  uint32_t forced[2];            // steps that are always up
+  uint32_t open[2];              // steps decided by the stream (valid and not forced)
   int N, r;
   unsigned kind;
   uint32_t key0, key1;

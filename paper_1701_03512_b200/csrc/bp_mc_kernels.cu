@@ -8,8 +8,14 @@
 // Stream layout (replaces numpy Philox(SeedSequence(seed, spawn_key=(m, rep)))):
 //   key     = (seed mod 2^32, seed >> 32)
 //   counter = (word block j, draw index i, stream id m, repetition)
-//   suffix step w (0-based after the r prefix steps) uses 32-bit word w % 4
-//   of block j = w / 4; up iff word < floor(p_t 2^32) (p_t == 1: always).
+//   suffix step w (0-based after the r prefix steps) is bit w % 32 of group
+//   g = w / 32.  Level l < 8 of group g is word (8 g + l) % 4 of block
+//   (8 g + l) / 4; the step's level-l bit is bit w % 32 of that word.  The
+//   8-bit string (level 0 first) is compared with the top 8 bits of
+//   thr_t = floor(p_t 2^32): smaller -> up, larger -> down, equal -> the
+//   step takes the draw's next tie word x (ties in ascending step order; tie
+//   word k is word k % 4 of block 4 + k / 4) and goes up iff
+//   x < (thr_t << 8) mod 2^32.  P(up) = thr_t / 2^32 exactly; p_t == 1: always.
 // Streams are disjoint by construction and independent of the thread
 // mapping, so results do not depend on the grid, the GPU count or timing.
 //
@@ -93,11 +99,7 @@ __device__ __forceinline__ double payoff_of(unsigned kind, const PathState& st, 
   }
 }
 
-// Walk the N - r suffix steps of draw i on stream (m, rep) from state st.
-// CONSTP: every suffix step has the same threshold thr0 (the BASELINE trees);
-// `up` is then one ISETP against a register (OR'ed with the uniform p == 1
-// flag) instead of a per-step table load.
-// Nibble tables: 4 consecutive steps with up-pattern b (step 1 = bit 3):
+// Nibble tables: 4 consecutive steps with up-pattern b (first step = bit 0):
 // relative price after the 4 steps (e), sum of the 4 relative prices (c),
 // their max (x) and min (n).  Built once per CTA in shared memory.
 struct Nib {
@@ -108,7 +110,7 @@ __device__ __forceinline__ void build_nib(const McArgs& a, Nib* nib) {
   for (int b = threadIdx.x; b < 16; b += blockDim.x) {
     double r = 1.0, c = 0.0, x = -INFINITY, n = INFINITY;
     for (int l = 0; l < 4; ++l) {
-      r *= ((b >> (3 - l)) & 1) ? a.u : a.d;
+      r *= ((b >> l) & 1) ? a.u : a.d;
       c += r;
       x = fmax(x, r);
       n = fmin(n, r);
@@ -117,101 +119,129 @@ __device__ __forceinline__ void build_nib(const McArgs& a, Nib* nib) {
   }
 }
 
-// Walk the N - r suffix steps of draw i on stream (m, rep) from state st.
-// Full blocks of 4 steps use the nibble tables (one Philox block -> 4
-// Bernoulli bits -> one table entry); the tail block walks step by step.
-// CONSTP: every suffix step has the same threshold thr0 (the BASELINE trees).
-template <unsigned KIND, bool CONSTP>
-__device__ __forceinline__ PathState walk_suffix(const McArgs& a, const Nib* __restrict__ nib, PathState st,
-                                                 uint32_t i, uint32_t stream, uint32_t rep, uint32_t thr0,
-                                                 bool all_up) {
-  constexpr bool need_max = KIND == kFL;
-  constexpr bool need_min = KIND == kFLP;
-  constexpr bool need_sum = KIND == kAC || KIND == kAP;
-  const int nsuf = a.N - a.r;
-  const int nfull = nsuf >> 2;
-  uint32_t blk[4];
-  auto up_of = [&](int w, uint32_t word) -> bool {
-    if (CONSTP) return (word < thr0) || all_up;
-    const int t = a.r + w;
-    return (word < a.thr[t]) || ((t < 32 ? (a.always[0] >> t) : (a.always[1] >> (t - 32))) & 1u);
-  };
-#pragma unroll 2
-  for (int j = 0; j < nfull; ++j) {
-    philox4x32_10((uint32_t)j, i, stream, rep, a.key0, a.key1, blk);
-    const unsigned b = ((unsigned)up_of(4 * j, blk[0]) << 3) | ((unsigned)up_of(4 * j + 1, blk[1]) << 2) |
-                       ((unsigned)up_of(4 * j + 2, blk[2]) << 1) | (unsigned)up_of(4 * j + 3, blk[3]);
-    const Nib q = nib[b];
-    if (need_sum) st.sum = fma(st.S, q.c, st.sum);
-    if (need_max) st.mx = fmax(st.mx, st.S * q.x);
-    if (need_min) st.mn = fmin(st.mn, st.S * q.n);
-    st.S *= q.e;
-  }
-  if (4 * nfull < nsuf) {
-    philox4x32_10((uint32_t)nfull, i, stream, rep, a.key0, a.key1, blk);
-#pragma unroll
-    for (int l = 0; l < 3; ++l) {
-      const int w = 4 * nfull + l;
-      if (w < nsuf) {
-        st.S *= up_of(w, blk[l]) ? a.u : a.d;
-        if (need_sum) st.sum += st.S;
-        if (need_max) st.mx = fmax(st.mx, st.S);
-        if (need_min) st.mn = fmin(st.mn, st.S);
-      }
-    }
-  }
-  return st;
-}
+constexpr uint32_t kMcPlaneBlocks = kMcLevels / 4;     // Philox blocks per group of 32 steps
+constexpr uint32_t kMcTieBlock0 = 2 * kMcPlaneBlocks;  // first block of the tie words
 
-// NS independent draws walked in lock step (the Philox rounds of the NS
-// counters interleave, giving the scheduler independent work) -- same bits
-// and same arithmetic per draw as walk_suffix.
-template <unsigned KIND, bool CONSTP, int NS>
-__device__ __forceinline__ void walk_suffix_n(const McArgs& a, const Nib* __restrict__ nib, PathState (&s)[NS],
-                                              uint32_t i0, uint32_t stride, uint32_t stream, uint32_t rep,
-                                              uint32_t thr0, bool all_up) {
-  constexpr bool need_max = KIND == kFL;
-  constexpr bool need_min = KIND == kFLP;
-  constexpr bool need_sum = KIND == kAC || KIND == kAP;
+// The up/down bits of the suffix steps of NS draws (i0, i0 + stride, ...) on
+// stream (m, rep): B[d][g] bit b = step 32 g + b of draw d goes up.
+//
+// Each step is Bernoulli(thr_t / 2^32), exactly, decided MSB-first against
+// the threshold's bits with the 32 steps of a group side by side in one
+// word: level l's word W gives every step one fair bit; a step whose bit
+// differs from the threshold's bit l is decided (up iff its bit is 0), the
+// others stay open.  After kMcLevels levels an open step (probability
+// 2^-kMcLevels) takes the next tie word x and goes up iff
+// x < (thr_t << kMcLevels) mod 2^32.  3 LOP3 per level and group instead of
+// a compare per step, and 5 Philox blocks per draw instead of one word per
+// step (13 blocks at 52 steps).
+template <int NS>
+__device__ __forceinline__ void draw_bits(const McArgs& a, uint32_t (&B)[NS][2], uint32_t i0, uint32_t stride,
+                                          uint32_t stream, uint32_t rep) {
   const int nsuf = a.N - a.r;
-  const int nfull = nsuf >> 2;
-  uint32_t blk[NS][4];
-  auto up_of = [&](int w, uint32_t word) -> bool {
-    if (CONSTP) return (word < thr0) || all_up;
-    const int t = a.r + w;
-    return (word < a.thr[t]) || ((t < 32 ? (a.always[0] >> t) : (a.always[1] >> (t - 32))) & 1u);
-  };
-  for (int j = 0; j < nfull; ++j) {
+  uint32_t U[NS][2], tie[NS][4];
 #pragma unroll
-    for (int d = 0; d < NS; ++d) philox4x32_10((uint32_t)j, i0 + d * stride, stream, rep, a.key0, a.key1, blk[d]);
+  for (int d = 0; d < NS; ++d)
+    philox4x32_10(kMcTieBlock0, i0 + d * stride, stream, rep, a.key0, a.key1, tie[d]);
+#pragma unroll
+  for (int g = 0; g < 2; ++g) {
 #pragma unroll
     for (int d = 0; d < NS; ++d) {
-      const unsigned b = ((unsigned)up_of(4 * j, blk[d][0]) << 3) | ((unsigned)up_of(4 * j + 1, blk[d][1]) << 2) |
-                         ((unsigned)up_of(4 * j + 2, blk[d][2]) << 1) | (unsigned)up_of(4 * j + 3, blk[d][3]);
-      const Nib q = nib[b];
-      if (need_sum) s[d].sum = fma(s[d].S, q.c, s[d].sum);
-      if (need_max) s[d].mx = fmax(s[d].mx, s[d].S * q.x);
-      if (need_min) s[d].mn = fmin(s[d].mn, s[d].S * q.n);
-      s[d].S *= q.e;
+      B[d][g] = a.forced[g];
+      U[d][g] = a.open[g];
     }
-  }
-  if (4 * nfull < nsuf) {
+    if (32 * g < nsuf) {
 #pragma unroll
-    for (int d = 0; d < NS; ++d) philox4x32_10((uint32_t)nfull, i0 + d * stride, stream, rep, a.key0, a.key1, blk[d]);
+      for (int jb = 0; jb < (int)kMcPlaneBlocks; ++jb) {
+        uint32_t blk[NS][4];
 #pragma unroll
-    for (int l = 0; l < 3; ++l) {
-      const int w = 4 * nfull + l;
-      if (w < nsuf) {
+        for (int d = 0; d < NS; ++d)
+          philox4x32_10(g * kMcPlaneBlocks + jb, i0 + d * stride, stream, rep, a.key0, a.key1, blk[d]);
 #pragma unroll
-        for (int d = 0; d < NS; ++d) {
-          s[d].S *= up_of(w, blk[d][l]) ? a.u : a.d;
-          if (need_sum) s[d].sum += s[d].S;
-          if (need_max) s[d].mx = fmax(s[d].mx, s[d].S);
-          if (need_min) s[d].mn = fmin(s[d].mn, s[d].S);
+        for (int l = 0; l < 4; ++l) {
+          const uint32_t T = a.tmask[g][4 * jb + l];
+#pragma unroll
+          for (int d = 0; d < NS; ++d) {
+            const uint32_t W = blk[d][l];
+            B[d][g] |= U[d][g] & ~W & T;
+            U[d][g] &= ~(W ^ T);
+          }
         }
       }
     }
   }
+  // ties, in ascending step order: tie word k of the draw is word k % 4 of
+  // block kMcTieBlock0 + k / 4
+#pragma unroll
+  for (int d = 0; d < NS; ++d) {
+    if ((U[d][0] | U[d][1]) == 0u) continue;
+    uint32_t k = 0;
+#pragma unroll
+    for (int g = 0; g < 2; ++g) {
+      uint32_t u = U[d][g];
+      while (u) {
+        const int b = __ffs((int)u) - 1;
+        u &= u - 1;
+        if (k >= 4u && (k & 3u) == 0u)
+          philox4x32_10(kMcTieBlock0 + (k >> 2), i0 + d * stride, stream, rep, a.key0, a.key1, tie[d]);
+        const uint32_t kk = k & 3u;
+        const uint32_t x = kk == 0u ? tie[d][0] : kk == 1u ? tie[d][1] : kk == 2u ? tie[d][2] : tie[d][3];
+        if (x < (a.thr[a.r + 32 * g + b] << kMcLevels)) B[d][g] |= 1u << b;
+        ++k;
+      }
+    }
+  }
+}
+
+// Walk the N - r suffix steps of NS draws in lock step from their states
+// (the Philox rounds of the NS counters interleave, giving the scheduler
+// independent work).  Full blocks of 4 steps use the nibble tables; the
+// tail walks step by step.
+template <unsigned KIND, int NS>
+__device__ __forceinline__ void walk_suffix_n(const McArgs& a, const Nib* __restrict__ nib, PathState (&s)[NS],
+                                              uint32_t i0, uint32_t stride, uint32_t stream, uint32_t rep) {
+  constexpr bool need_max = KIND == kFL;
+  constexpr bool need_min = KIND == kFLP;
+  constexpr bool need_sum = KIND == kAC || KIND == kAP;
+  const int nsuf = a.N - a.r;
+  const int nfull = nsuf >> 2;
+  uint32_t B[NS][2];
+  draw_bits<NS>(a, B, i0, stride, stream, rep);
+#pragma unroll
+  for (int g = 0; g < 2; ++g) {
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+      if (8 * g + jj < nfull) {
+#pragma unroll
+        for (int d = 0; d < NS; ++d) {
+          // byte offset of entry (B >> 4 jj) & 15 in the 32-byte-entry table
+          const uint32_t off = (4 * jj >= 5 ? B[d][g] >> (4 * jj - 5) : B[d][g] << (5 - 4 * jj)) & 0x1E0u;
+          const Nib* q = reinterpret_cast<const Nib*>(reinterpret_cast<const char*>(nib) + off);
+          if (need_sum) s[d].sum = fma(s[d].S, q->c, s[d].sum);
+          if (need_max) s[d].mx = fmax(s[d].mx, s[d].S * q->x);
+          if (need_min) s[d].mn = fmin(s[d].mn, s[d].S * q->n);
+          s[d].S *= q->e;
+        }
+      }
+    }
+  }
+  for (int w = 4 * nfull; w < nsuf; ++w) {
+#pragma unroll
+    for (int d = 0; d < NS; ++d) {
+      const uint32_t word = (w >> 5) ? B[d][1] : B[d][0];
+      s[d].S *= ((word >> (w & 31)) & 1u) ? a.u : a.d;
+      if (need_sum) s[d].sum += s[d].S;
+      if (need_max) s[d].mx = fmax(s[d].mx, s[d].S);
+      if (need_min) s[d].mn = fmin(s[d].mn, s[d].S);
+    }
+  }
+}
+
+template <unsigned KIND>
+__device__ __forceinline__ PathState walk_suffix(const McArgs& a, const Nib* __restrict__ nib, PathState st, uint32_t i,
+                                                 uint32_t stream, uint32_t rep) {
+  PathState s[1] = {st};
+  walk_suffix_n<KIND, 1>(a, nib, s, i, 0u, stream, rep);
+  return s[0];
 }
 
 #ifndef BP_MC_NS
@@ -243,7 +273,7 @@ struct ShiftedSums {
 #ifndef BP_MC_MINB
 #define BP_MC_MINB 1  // resident CTAs per SM targeted by K4 (1: no register cap)
 #endif
-template <unsigned KIND, bool CONSTP>
+template <unsigned KIND>
 __global__ void __launch_bounds__(kMcThreads, BP_MC_MINB)
 k_mc_strata(const __grid_constant__ McArgs a, const unsigned long long* __restrict__ draws,
             const unsigned long long* __restrict__ item_stratum, const unsigned long long* __restrict__ item_first,
@@ -252,8 +282,6 @@ k_mc_strata(const __grid_constant__ McArgs a, const unsigned long long* __restri
   build_nib(a, nib);
   __syncthreads();
   const unsigned long long n_items = items_per_rep * (unsigned long long)n_reps;
-  const uint32_t thr0 = a.thr[a.r < a.N ? a.r : 0];
-  const bool all_up = (a.always[0] | a.always[1]) != 0u;
   for (unsigned long long it = blockIdx.x; it < n_items; it += gridDim.x) {
     const unsigned long long k = it / items_per_rep, li = it % items_per_rep;
     const unsigned long long m = item_stratum[li];
@@ -270,21 +298,18 @@ k_mc_strata(const __grid_constant__ McArgs a, const unsigned long long* __restri
       PathState sd[kMcNS];
 #pragma unroll
       for (int d = 0; d < kMcNS; ++d) sd[d] = pre;
-      walk_suffix_n<KIND, CONSTP, kMcNS>(a, nib, sd, (uint32_t)i, kMcThreads, (uint32_t)m, a.rep0 + (uint32_t)k,
-                                         thr0, all_up);
+      walk_suffix_n<KIND, kMcNS>(a, nib, sd, (uint32_t)i, kMcThreads, (uint32_t)m, a.rep0 + (uint32_t)k);
 #pragma unroll
       for (int d = 0; d < kMcNS; ++d) acc.add(payoff_of(KIND, sd[d], a.K, a.N));
     }
     for (; kMcNS > 2 && i + kMcThreads < last; i += 2 * kMcThreads) {
       PathState sd[2] = {pre, pre};
-      walk_suffix_n<KIND, CONSTP, 2>(a, nib, sd, (uint32_t)i, kMcThreads, (uint32_t)m, a.rep0 + (uint32_t)k, thr0,
-                                     all_up);
+      walk_suffix_n<KIND, 2>(a, nib, sd, (uint32_t)i, kMcThreads, (uint32_t)m, a.rep0 + (uint32_t)k);
       acc.add(payoff_of(KIND, sd[0], a.K, a.N));
       acc.add(payoff_of(KIND, sd[1], a.K, a.N));
     }
     if (i < last) {
-      const PathState st = walk_suffix<KIND, CONSTP>(a, nib, pre, (uint32_t)i, (uint32_t)m, a.rep0 + (uint32_t)k, thr0,
-                                                     all_up);
+      const PathState st = walk_suffix<KIND>(a, nib, pre, (uint32_t)i, (uint32_t)m, a.rep0 + (uint32_t)k);
       acc.add(payoff_of(KIND, st, a.K, a.N));
     }
     const Welford t = cta_merge(acc.welford());
@@ -323,23 +348,12 @@ cudaError_t launch_mc_strata(const McArgs& a, const unsigned long long* draws_de
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const unsigned long long n_items = items_per_rep * (unsigned long long)n_reps;
-  bool constp = true;  // one threshold for every suffix step (and one p == 1 flag)
-  for (int t = a.r; t < a.N; ++t) constp = constp && a.thr[t] == a.thr[a.r];
-  {
-    const bool any = (a.always[0] | a.always[1]) != 0u;
-    for (int t = a.r; t < a.N && any; ++t)
-      constp = constp && (((t < 32 ? a.always[0] >> t : a.always[1] >> (t - 32)) & 1u) != 0u);
-  }
   if (n_items) {
     const int grid = (int)(n_items < (unsigned long long)sms * 16 ? n_items : (unsigned long long)sms * 16);
 #define BP_MC_CASE(K)                                                                                         \
   case K:                                                                                                     \
-    if (constp)                                                                                               \
-      k_mc_strata<K, true><<<grid, kMcThreads, 0, st>>>(a, draws_dev, item_stratum_dev, item_first_dev,       \
-                                                         items_per_rep, n_reps, item_out_dev);                 \
-    else                                                                                                      \
-      k_mc_strata<K, false><<<grid, kMcThreads, 0, st>>>(a, draws_dev, item_stratum_dev, item_first_dev,      \
-                                                          items_per_rep, n_reps, item_out_dev);                \
+    k_mc_strata<K><<<grid, kMcThreads, 0, st>>>(a, draws_dev, item_stratum_dev, item_first_dev, items_per_rep, \
+                                                n_reps, item_out_dev);                                         \
     break;
     switch (a.kind) {
       BP_MC_CASE(kEC) BP_MC_CASE(kEP) BP_MC_CASE(kAP) BP_MC_CASE(kFLP) BP_MC_CASE(kAC) BP_MC_CASE(kFL)
@@ -384,7 +398,7 @@ k_mc_shared(const __grid_constant__ McArgs a, unsigned long long R, const double
       const bool live = i < last;
       // suffix relative to a unit start price
       PathState rel{1.0, 0.0, -INFINITY, INFINITY};
-      if (live) rel = walk_suffix<KIND, false>(a, nib, rel, (uint32_t)i, 0u, a.rep0 + (uint32_t)k, 0u, false);
+      if (live) rel = walk_suffix<KIND>(a, nib, rel, (uint32_t)i, 0u, a.rep0 + (uint32_t)k);
       double inner = 0.0;
       for (int m = 0; m < M; ++m) {
         const double S = pre_tab[4 * m], sum = pre_tab[4 * m + 1], mx = pre_tab[4 * m + 2], mn = pre_tab[4 * m + 3];

@@ -87,8 +87,8 @@ class RepetitionSummary:
 
 # ---------------------------------------------------------------------------
 class PhiloxStream:
-    """Host view of the engine's stream (seed, stratum, rep): uniforms in
-    [0, 1) with 32-bit resolution, word w of draw i = block w//4, lane w%4.
+    """Host view of the engine's stream (seed, stratum, rep): word q of draw
+    i = Philox block q//4, lane q%4; bits() applies the engine's sampler.
     Mirrors mc_stream's role (mc.py:92-95) for inspection and tests; the
     estimators draw on the GPU."""
 
@@ -107,14 +107,42 @@ class PhiloxStream:
             out[4 * j:4 * j + n] = list(blk)[:n]
         return out
 
+    LEVELS = 8  # threshold bits compared bit-sliced before the tie words (csrc/bp_mc_kernels.cu)
+
     def bits(self, probs: np.ndarray) -> np.ndarray:
-        """Next draw's Bernoulli bits, bit t up with probability probs[t]."""
+        """Next draw's Bernoulli bits, bit t up with probability probs[t]
+        (floor(p 2^32) / 2^32), by the engine's sampler with no fixed prefix:
+        step w is bit w % 32 of group w // 32; its 8 level bits (word
+        8 g + l, l = 0 first) against the top 8 bits of the threshold decide
+        it unless they are equal, then the draw's next tie word (word 16 + k)
+        does against the threshold's low 24 bits."""
         probs = np.asarray(probs, dtype=np.float64)
-        w = self.words(self._draw, probs.shape[0]).astype(np.uint64)
-        self._draw += 1
-        thr = np.where(probs >= 1.0, np.uint64(1 << 32), np.floor(np.clip(probs, 0.0, 1.0) * 4294967296.0)
-                       .astype(np.uint64))
-        return w < thr
+        n = probs.shape[0]
+        if n > 64:
+            raise InvalidInput("the sampler draws at most 64 steps")
+        L = self.LEVELS
+        draw, self._draw = self._draw, self._draw + 1
+        planes = [int(x) for x in self.words(draw, 2 * L)]
+        up = np.zeros(n, dtype=bool)
+        k = 0
+        for w in range(n):
+            p = float(probs[w])
+            if p >= 1.0:
+                up[w] = True
+                continue
+            thr = int(math.floor(min(max(p, 0.0), 1.0) * 4294967296.0))
+            g, b = divmod(w, 32)
+            s = 0
+            for lvl in range(L):
+                s = (s << 1) | ((planes[L * g + lvl] >> b) & 1)
+            top = thr >> (32 - L)
+            if s != top:
+                up[w] = s < top
+                continue
+            x = int(self.words(draw, 2 * L + k + 1)[2 * L + k])
+            up[w] = x < ((thr << L) & 0xFFFFFFFF)
+            k += 1
+        return up
 
     def random(self, size: int) -> np.ndarray:
         """Uniforms of one draw's words (32-bit resolution)."""

@@ -103,3 +103,38 @@ def test_mc_oracle_single_stratum_equals_basic_and_is_unbiased():
     # variance estimate calibrated against the empirical spread (20 %, test_mc.py:317-325)
     mean_var = np.mean(disc * disc * sse[:, 0] / 512 ** 2)
     assert mean_var == pytest.approx(vals.var(ddof=1), rel=0.25)
+
+
+# ---------------------------------------------------------------------------
+# The sampler (csrc/bp_mc_kernels.cu header; replaces sample_bits, mc.py:98-100)
+def test_sampler_host_view_matches_oracle_bits():
+    """PhiloxStream.bits (host view of the engine's stream) and the oracle's
+    step-by-step restatement of the sampler give the same bits, for steps in
+    both 32-step groups, forced steps (p = 1), p = 0 and thresholds whose top
+    byte ties often."""
+    import paper_1701_03512_b200 as bp
+    rng = np.random.default_rng(5)
+    for N in (1, 7, 32, 33, 52, 64):
+        probs = rng.uniform(0.0, 1.0, N)
+        probs[::5] = 0.5 + 2.0 ** -20  # the top 8 bits tie with probability 2^-8
+        if N > 3:
+            probs[1], probs[3] = 1.0, 0.0
+        for stream, rep in ((0, 0), (11, 3)):
+            host = bp.mc_stream(1234567890123, stream, rep)
+            for draw in range(40):
+                want = oracle.mc_bits(N, 0, probs, 1234567890123, stream, rep, draw)
+                got = host.bits(probs)
+                assert np.array_equal(got, want), (N, stream, rep, draw)
+
+
+def test_sampler_frequencies_match_the_thresholds():
+    """Each step is Bernoulli(floor(p 2^32) / 2^32): up-frequencies over 2^16
+    draws stay within 5 sigma of p, including a threshold of 2^-8 + 2^-9 (the
+    tie words carry half its mass) and one below 2^-8 (all of it)."""
+    probs = np.array([0.5, 0.5077, 2.0 ** -8 + 2.0 ** -9, 2.0 ** -10, 0.999, 0.25, 1.0 - 2.0 ** -9, 0.75] * 5)
+    N, R = probs.shape[0], 1 << 16
+    ups = np.zeros(N)
+    for draw in range(R):
+        ups += oracle.mc_bits(N, 0, probs, 99, 2, 1, draw)
+    sigma = np.sqrt(probs * (1 - probs) / R)
+    assert np.all(np.abs(ups / R - probs) <= 5 * sigma), (ups / R - probs) / sigma
