@@ -13,9 +13,10 @@
 //   (8 g + l) / 4; the step's level-l bit is bit w % 32 of that word.  The
 //   8-bit string (level 0 first) is compared with the top 8 bits of
 //   thr_t = floor(p_t 2^32): smaller -> up, larger -> down, equal -> the
-//   step takes the draw's next tie word x (ties in ascending step order; tie
-//   word k is word k % 4 of block 4 + k / 4) and goes up iff
-//   x < (thr_t << 8) mod 2^32.  P(up) = thr_t / 2^32 exactly; p_t == 1: always.
+//   step takes its group's next tie word x (the k-th tie of group g in
+//   ascending step order: word q = 2 k + g of the tie stream, i.e. word
+//   q % 4 of block 4 + q / 4) and goes up iff x < (thr_t << 8) mod 2^32.
+//   P(up) = thr_t / 2^32 exactly; p_t == 1: always.
 // Streams are disjoint by construction and independent of the thread
 // mapping, so results do not depend on the grid, the GPU count or timing.
 //
@@ -87,8 +88,8 @@ __device__ __forceinline__ PathState prefix_state(const McArgs& a, unsigned long
   return st;
 }
 
-__device__ __forceinline__ double payoff_of(unsigned kind, const PathState& st, double K, int N) {
-  const double mean = st.sum / (double)N;
+__device__ __forceinline__ double payoff_of(unsigned kind, const PathState& st, double K, double invN) {
+  const double mean = st.sum * invN;
   switch (kind) {
     case kEC: return fmax(st.S - K, 0.0);
     case kEP: return fmax(K - st.S, 0.0);
@@ -130,18 +131,48 @@ constexpr uint32_t kMcTieBlock0 = 2 * kMcPlaneBlocks;  // first block of the tie
 // word: level l's word W gives every step one fair bit; a step whose bit
 // differs from the threshold's bit l is decided (up iff its bit is 0), the
 // others stay open.  After kMcLevels levels an open step (probability
-// 2^-kMcLevels) takes the next tie word x and goes up iff
+// 2^-kMcLevels) takes the group's next tie word x and goes up iff
 // x < (thr_t << kMcLevels) mod 2^32.  3 LOP3 per level and group instead of
 // a compare per step, and 5 Philox blocks per draw instead of one word per
 // step (13 blocks at 52 steps).
-template <int NS>
+//
+// Tie words: the k-th open step of group g (ascending) takes word
+// q = 2 k + g of the tie stream, word q % 4 of block kMcTieBlock0 + q / 4,
+// so each group's first two ties are served by the one block every draw
+// computes.  CONSTP (every suffix step has the same threshold): the first
+// tie of a group needs no bit search -- the lowest open bit u & -u goes up
+// iff its word is below the common tie threshold.
+template <bool CONSTP, int G>
+__device__ __forceinline__ void resolve_ties(const McArgs& a, uint32_t& Bg, uint32_t u, const uint32_t (&tie)[4],
+                                             uint32_t thr_tie, uint32_t draw, uint32_t stream, uint32_t rep) {
+  auto tie_thr = [&](uint32_t low) -> uint32_t {
+    if (CONSTP) return thr_tie;
+    return a.thr[a.r + 32 * G + (__ffs((int)low) - 1)] << kMcLevels;
+  };
+  if (CONSTP) {
+    if (tie[G] < thr_tie) Bg |= u & (0u - u);
+  } else if (u) {
+    const uint32_t low = u & (0u - u);
+    if (tie[G] < tie_thr(low)) Bg |= low;
+  }
+  u &= u - 1u;
+  if (u == 0u) return;
+  // second and later ties of the group (about 1 draw in 150)
+  uint32_t blk[4] = {tie[0], tie[1], tie[2], tie[3]};
+  for (uint32_t k = 1; u; ++k, u &= u - 1u) {
+    const uint32_t q = 2u * k + G;
+    if ((q & 3u) == (uint32_t)G) philox4x32_10(kMcTieBlock0 + (q >> 2), draw, stream, rep, a.key0, a.key1, blk);
+    const uint32_t x = (q & 2u) ? blk[2 + G] : blk[G];
+    const uint32_t low = u & (0u - u);
+    if (x < tie_thr(low)) Bg |= low;
+  }
+}
+
+template <bool CONSTP, int NS>
 __device__ __forceinline__ void draw_bits(const McArgs& a, uint32_t (&B)[NS][2], uint32_t i0, uint32_t stride,
                                           uint32_t stream, uint32_t rep) {
   const int nsuf = a.N - a.r;
-  uint32_t U[NS][2], tie[NS][4];
-#pragma unroll
-  for (int d = 0; d < NS; ++d)
-    philox4x32_10(kMcTieBlock0, i0 + d * stride, stream, rep, a.key0, a.key1, tie[d]);
+  uint32_t U[NS][2];
 #pragma unroll
   for (int g = 0; g < 2; ++g) {
 #pragma unroll
@@ -169,26 +200,15 @@ __device__ __forceinline__ void draw_bits(const McArgs& a, uint32_t (&B)[NS][2],
       }
     }
   }
-  // ties, in ascending step order: tie word k of the draw is word k % 4 of
-  // block kMcTieBlock0 + k / 4
+  const uint32_t thr_tie = a.thr[a.r < a.N ? a.r : 0] << kMcLevels;
+  uint32_t tie[NS][4];
+#pragma unroll
+  for (int d = 0; d < NS; ++d)
+    philox4x32_10(kMcTieBlock0, i0 + d * stride, stream, rep, a.key0, a.key1, tie[d]);
 #pragma unroll
   for (int d = 0; d < NS; ++d) {
-    if ((U[d][0] | U[d][1]) == 0u) continue;
-    uint32_t k = 0;
-#pragma unroll
-    for (int g = 0; g < 2; ++g) {
-      uint32_t u = U[d][g];
-      while (u) {
-        const int b = __ffs((int)u) - 1;
-        u &= u - 1;
-        if (k >= 4u && (k & 3u) == 0u)
-          philox4x32_10(kMcTieBlock0 + (k >> 2), i0 + d * stride, stream, rep, a.key0, a.key1, tie[d]);
-        const uint32_t kk = k & 3u;
-        const uint32_t x = kk == 0u ? tie[d][0] : kk == 1u ? tie[d][1] : kk == 2u ? tie[d][2] : tie[d][3];
-        if (x < (a.thr[a.r + 32 * g + b] << kMcLevels)) B[d][g] |= 1u << b;
-        ++k;
-      }
-    }
+    resolve_ties<CONSTP, 0>(a, B[d][0], U[d][0], tie[d], thr_tie, i0 + d * stride, stream, rep);
+    resolve_ties<CONSTP, 1>(a, B[d][1], U[d][1], tie[d], thr_tie, i0 + d * stride, stream, rep);
   }
 }
 
@@ -196,7 +216,7 @@ __device__ __forceinline__ void draw_bits(const McArgs& a, uint32_t (&B)[NS][2],
 // (the Philox rounds of the NS counters interleave, giving the scheduler
 // independent work).  Full blocks of 4 steps use the nibble tables; the
 // tail walks step by step.
-template <unsigned KIND, int NS>
+template <unsigned KIND, bool CONSTP, int NS>
 __device__ __forceinline__ void walk_suffix_n(const McArgs& a, const Nib* __restrict__ nib, PathState (&s)[NS],
                                               uint32_t i0, uint32_t stride, uint32_t stream, uint32_t rep) {
   constexpr bool need_max = KIND == kFL;
@@ -205,7 +225,7 @@ __device__ __forceinline__ void walk_suffix_n(const McArgs& a, const Nib* __rest
   const int nsuf = a.N - a.r;
   const int nfull = nsuf >> 2;
   uint32_t B[NS][2];
-  draw_bits<NS>(a, B, i0, stride, stream, rep);
+  draw_bits<CONSTP, NS>(a, B, i0, stride, stream, rep);
 #pragma unroll
   for (int g = 0; g < 2; ++g) {
 #pragma unroll
@@ -236,11 +256,11 @@ __device__ __forceinline__ void walk_suffix_n(const McArgs& a, const Nib* __rest
   }
 }
 
-template <unsigned KIND>
+template <unsigned KIND, bool CONSTP>
 __device__ __forceinline__ PathState walk_suffix(const McArgs& a, const Nib* __restrict__ nib, PathState st, uint32_t i,
                                                  uint32_t stream, uint32_t rep) {
   PathState s[1] = {st};
-  walk_suffix_n<KIND, 1>(a, nib, s, i, 0u, stream, rep);
+  walk_suffix_n<KIND, CONSTP, 1>(a, nib, s, i, 0u, stream, rep);
   return s[0];
 }
 
@@ -271,9 +291,9 @@ struct ShiftedSums {
 // ---------------------------------------------------------------------------
 // K4/K5: one CTA per work item (grid-stride).  item -> (rep k, stratum m, first draw)
 #ifndef BP_MC_MINB
-#define BP_MC_MINB 1  // resident CTAs per SM targeted by K4 (1: no register cap)
+#define BP_MC_MINB 4  // resident CTAs per SM targeted by K4 (r2 scan with the bit-sliced sampler: 1-3 lose 7-20 %)
 #endif
-template <unsigned KIND>
+template <unsigned KIND, bool CONSTP>
 __global__ void __launch_bounds__(kMcThreads, BP_MC_MINB)
 k_mc_strata(const __grid_constant__ McArgs a, const unsigned long long* __restrict__ draws,
             const unsigned long long* __restrict__ item_stratum, const unsigned long long* __restrict__ item_first,
@@ -298,19 +318,19 @@ k_mc_strata(const __grid_constant__ McArgs a, const unsigned long long* __restri
       PathState sd[kMcNS];
 #pragma unroll
       for (int d = 0; d < kMcNS; ++d) sd[d] = pre;
-      walk_suffix_n<KIND, kMcNS>(a, nib, sd, (uint32_t)i, kMcThreads, (uint32_t)m, a.rep0 + (uint32_t)k);
+      walk_suffix_n<KIND, CONSTP, kMcNS>(a, nib, sd, (uint32_t)i, kMcThreads, (uint32_t)m, a.rep0 + (uint32_t)k);
 #pragma unroll
-      for (int d = 0; d < kMcNS; ++d) acc.add(payoff_of(KIND, sd[d], a.K, a.N));
+      for (int d = 0; d < kMcNS; ++d) acc.add(payoff_of(KIND, sd[d], a.K, a.invN));
     }
     for (; kMcNS > 2 && i + kMcThreads < last; i += 2 * kMcThreads) {
       PathState sd[2] = {pre, pre};
-      walk_suffix_n<KIND, 2>(a, nib, sd, (uint32_t)i, kMcThreads, (uint32_t)m, a.rep0 + (uint32_t)k);
-      acc.add(payoff_of(KIND, sd[0], a.K, a.N));
-      acc.add(payoff_of(KIND, sd[1], a.K, a.N));
+      walk_suffix_n<KIND, CONSTP, 2>(a, nib, sd, (uint32_t)i, kMcThreads, (uint32_t)m, a.rep0 + (uint32_t)k);
+      acc.add(payoff_of(KIND, sd[0], a.K, a.invN));
+      acc.add(payoff_of(KIND, sd[1], a.K, a.invN));
     }
     if (i < last) {
-      const PathState st = walk_suffix<KIND>(a, nib, pre, (uint32_t)i, (uint32_t)m, a.rep0 + (uint32_t)k);
-      acc.add(payoff_of(KIND, st, a.K, a.N));
+      const PathState st = walk_suffix<KIND, CONSTP>(a, nib, pre, (uint32_t)i, (uint32_t)m, a.rep0 + (uint32_t)k);
+      acc.add(payoff_of(KIND, st, a.K, a.invN));
     }
     const Welford t = cta_merge(acc.welford());
     if (threadIdx.x == 0) {
@@ -348,12 +368,20 @@ cudaError_t launch_mc_strata(const McArgs& a, const unsigned long long* draws_de
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const unsigned long long n_items = items_per_rep * (unsigned long long)n_reps;
+  // one threshold for every stream-decided suffix step (the BASELINE trees)
+  bool constp = a.r < a.N && !((a.always[a.r / 32] >> (a.r % 32)) & 1u);
+  for (int t = a.r; t < a.N && constp; ++t)
+    if (!((a.always[t / 32] >> (t % 32)) & 1u)) constp = a.thr[t] == a.thr[a.r];
   if (n_items) {
     const int grid = (int)(n_items < (unsigned long long)sms * 16 ? n_items : (unsigned long long)sms * 16);
 #define BP_MC_CASE(K)                                                                                         \
   case K:                                                                                                     \
-    k_mc_strata<K><<<grid, kMcThreads, 0, st>>>(a, draws_dev, item_stratum_dev, item_first_dev, items_per_rep, \
-                                                n_reps, item_out_dev);                                         \
+    if (constp)                                                                                               \
+      k_mc_strata<K, true><<<grid, kMcThreads, 0, st>>>(a, draws_dev, item_stratum_dev, item_first_dev,       \
+                                                         items_per_rep, n_reps, item_out_dev);                 \
+    else                                                                                                      \
+      k_mc_strata<K, false><<<grid, kMcThreads, 0, st>>>(a, draws_dev, item_stratum_dev, item_first_dev,      \
+                                                          items_per_rep, n_reps, item_out_dev);                \
     break;
     switch (a.kind) {
       BP_MC_CASE(kEC) BP_MC_CASE(kEP) BP_MC_CASE(kAP) BP_MC_CASE(kFLP) BP_MC_CASE(kAC) BP_MC_CASE(kFL)
@@ -398,12 +426,12 @@ k_mc_shared(const __grid_constant__ McArgs a, unsigned long long R, const double
       const bool live = i < last;
       // suffix relative to a unit start price
       PathState rel{1.0, 0.0, -INFINITY, INFINITY};
-      if (live) rel = walk_suffix<KIND>(a, nib, rel, (uint32_t)i, 0u, a.rep0 + (uint32_t)k);
+      if (live) rel = walk_suffix<KIND, false>(a, nib, rel, (uint32_t)i, 0u, a.rep0 + (uint32_t)k);
       double inner = 0.0;
       for (int m = 0; m < M; ++m) {
         const double S = pre_tab[4 * m], sum = pre_tab[4 * m + 1], mx = pre_tab[4 * m + 2], mn = pre_tab[4 * m + 3];
         PathState st{S * rel.S, fma(S, rel.sum, sum), fmax(mx, S * rel.mx), fmin(mn, S * rel.mn)};
-        const double v = live ? payoff_of(KIND, st, a.K, a.N) : 0.0;
+        const double v = live ? payoff_of(KIND, st, a.K, a.invN) : 0.0;
         inner = fma(masses[m], v, inner);
         double s = v;
 #pragma unroll

@@ -114,8 +114,9 @@ class PhiloxStream:
         (floor(p 2^32) / 2^32), by the engine's sampler with no fixed prefix:
         step w is bit w % 32 of group w // 32; its 8 level bits (word
         8 g + l, l = 0 first) against the top 8 bits of the threshold decide
-        it unless they are equal, then the draw's next tie word (word 16 + k)
-        does against the threshold's low 24 bits."""
+        it unless they are equal, then the group's next tie word (the k-th
+        tie of group g: word 16 + 2 k + g) does against the threshold's low
+        24 bits."""
         probs = np.asarray(probs, dtype=np.float64)
         n = probs.shape[0]
         if n > 64:
@@ -124,7 +125,7 @@ class PhiloxStream:
         draw, self._draw = self._draw, self._draw + 1
         planes = [int(x) for x in self.words(draw, 2 * L)]
         up = np.zeros(n, dtype=bool)
-        k = 0
+        ties = [0, 0]
         for w in range(n):
             p = float(probs[w])
             if p >= 1.0:
@@ -139,9 +140,10 @@ class PhiloxStream:
             if s != top:
                 up[w] = s < top
                 continue
-            x = int(self.words(draw, 2 * L + k + 1)[2 * L + k])
+            q = 2 * L + 2 * ties[g] + g
+            x = int(self.words(draw, q + 1)[q])
             up[w] = x < ((thr << L) & 0xFFFFFFFF)
-            k += 1
+            ties[g] += 1
         return up
 
     def random(self, size: int) -> np.ndarray:
