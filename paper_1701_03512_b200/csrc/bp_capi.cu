@@ -1625,17 +1625,21 @@ static void fill_mc_args(const bp_tree* t, unsigned kind, int r, uint64_t seed, 
     }
     a.thr[i] = thr;
   }
-  // the sampler's bit planes: suffix step w = i - r sits at bit w % 32 of group w / 32
+  // the sampler's bit planes: suffix step w = i - r sits at bit w % 32 of group w / 32;
+  // T_l = threshold bit 31 - l (l < kMcLevels), up set = XOR_l (U_l & (T_{l-1} ^ T_l)) with
+  // T_{-1} = T_{kMcLevels} = 0 (bp_mc_kernels.cu, draw_bits)
   for (int i = r; i < t->n_steps; ++i) {
     const int w = i - r, g = w >> 5;
     const uint32_t bit = 1u << (w & 31);
     if ((a.always[i / 32] >> (i % 32)) & 1u) {
-      a.forced[g] |= bit;
+      a.bits0[g] |= bit;
       continue;
     }
     a.open[g] |= bit;
+    auto T = [&](int l) -> uint32_t { return l < 0 || l >= kMcLevels ? 0u : (a.thr[i] >> (31 - l)) & 1u; };
+    if (T(0)) a.bits0[g] |= bit;
     for (int l = 0; l < kMcLevels; ++l)
-      if ((a.thr[i] >> (31 - l)) & 1u) a.tmask[g][l] |= bit;
+      if (T(l) ^ T(l + 1)) a.flip[g][l] |= bit;
   }
 }
 

@@ -51,9 +51,9 @@ struct McArgs {
   uint32_t thr[kMaxN];   // Bernoulli thresholds floor(p_t 2^32) (saturated)
   uint32_t always[2];    // bit t set: step t is always up (p_t >= 1)
   // bit-sliced sampler (bp_mc_kernels.cu): suffix step w = 32 g + b is bit b of group g
-  uint32_t tmask[2][kMcLevels];  // level i: bit b = bit (31 - i) of the step's threshold
-  uint32_t forced[2];            // steps that are always up
-  uint32_t open[2];              // steps decided by the stream (valid and not forced)
+  uint32_t flip[2][kMcLevels];  // C_{l+1}: steps whose threshold bits 31 - l and 30 - l differ (bit -1 = 0)
+  uint32_t bits0[2];            // steps that are always up, and U_0 & C_0 (threshold bit 31 set)
+  uint32_t open[2];             // U_0: steps decided by the stream (valid and not forced)
   int N, r;
   unsigned kind;
   uint32_t key0, key1;

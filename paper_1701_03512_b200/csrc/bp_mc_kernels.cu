@@ -11,12 +11,13 @@
 //   suffix step w (0-based after the r prefix steps) is bit w % 32 of group
 //   g = w / 32.  Level l < 8 of group g is word (8 g + l) % 4 of block
 //   (8 g + l) / 4; the step's level-l bit is bit w % 32 of that word.  The
-//   8-bit string (level 0 first) is compared with the top 8 bits of
-//   thr_t = floor(p_t 2^32): smaller -> up, larger -> down, equal -> the
-//   step takes its group's next tie word x (the k-th tie of group g in
-//   ascending step order: word q = 2 k + g of the tie stream, i.e. word
-//   q % 4 of block 4 + q / 4) and goes up iff x < (thr_t << 8) mod 2^32.
-//   P(up) = thr_t / 2^32 exactly; p_t == 1: always.
+//   first level whose bit is 1 decides the step: up iff bit (31 - l) of
+//   thr_t = floor(p_t 2^32) is 1 (level l is first with probability
+//   2^-(l+1), so P(up) so far is the top 8 bits of thr_t).  A step with no 1
+//   in 8 levels (probability 2^-8) takes its group's next tie word x (the
+//   k-th such step of group g in ascending order: word q = 2 k + g of the tie
+//   stream, i.e. word q % 4 of block 4 + q / 4) and goes up iff
+//   x < (thr_t << 8) mod 2^32.  P(up) = thr_t / 2^32 exactly; p_t == 1: always.
 // Streams are disjoint by construction and independent of the thread
 // mapping, so results do not depend on the grid, the GPU count or timing.
 //
@@ -100,23 +101,32 @@ __device__ __forceinline__ double payoff_of(unsigned kind, const PathState& st, 
   }
 }
 
-// Nibble tables: 4 consecutive steps with up-pattern b (first step = bit 0):
-// relative price after the 4 steps (e), sum of the 4 relative prices (c),
-// their max (x) and min (n).  Built once per CTA in shared memory.
+// Step tables in shared memory.  Byte table: 8 consecutive steps with
+// up-pattern b (first step = bit 0): relative price after the 8 steps (e),
+// sum of the 8 relative prices (c) in ec[b]; their max (x) and min (n) in
+// xn[b].  The nibble table holds the same for 4 steps (the leftover nibble of
+// a suffix that is not a multiple of 8 steps).  Built once per CTA.
 struct Nib {
   double e, c, x, n;
 };
+struct McTables {
+  double2 ec[256];
+  double2 xn[256];
+  Nib nib[16];
+};
 
-__device__ __forceinline__ void build_nib(const McArgs& a, Nib* nib) {
-  for (int b = threadIdx.x; b < 16; b += blockDim.x) {
+__device__ __forceinline__ void build_tables(const McArgs& a, McTables& t) {
+  for (int b = threadIdx.x; b < 256; b += blockDim.x) {
     double r = 1.0, c = 0.0, x = -INFINITY, n = INFINITY;
-    for (int l = 0; l < 4; ++l) {
+    for (int l = 0; l < 8; ++l) {
       r *= ((b >> l) & 1) ? a.u : a.d;
       c += r;
       x = fmax(x, r);
       n = fmin(n, r);
+      if (l == 3 && b < 16) t.nib[b] = Nib{r, c, x, n};
     }
-    nib[b] = Nib{r, c, x, n};
+    t.ec[b] = make_double2(r, c);
+    t.xn[b] = make_double2(x, n);
   }
 }
 
@@ -126,15 +136,16 @@ constexpr uint32_t kMcTieBlock0 = 2 * kMcPlaneBlocks;  // first block of the tie
 // The up/down bits of the suffix steps of NS draws (i0, i0 + stride, ...) on
 // stream (m, rep): B[d][g] bit b = step 32 g + b of draw d goes up.
 //
-// Each step is Bernoulli(thr_t / 2^32), exactly, decided MSB-first against
-// the threshold's bits with the 32 steps of a group side by side in one
-// word: level l's word W gives every step one fair bit; a step whose bit
-// differs from the threshold's bit l is decided (up iff its bit is 0), the
-// others stay open.  After kMcLevels levels an open step (probability
-// 2^-kMcLevels) takes the group's next tie word x and goes up iff
-// x < (thr_t << kMcLevels) mod 2^32.  3 LOP3 per level and group instead of
-// a compare per step, and 5 Philox blocks per draw instead of one word per
-// step (13 blocks at 52 steps).
+// Each step is Bernoulli(thr_t / 2^32), exactly: level l's word gives every
+// one of the 32 steps of a group a fair bit, the first level whose bit is 1
+// decides the step (up iff the threshold's bit 31 - l is 1), the others stay
+// open.  The open sets U_0 > U_1 > ... are nested, so the up set is
+// XOR_l (U_l & C_l) with C_l = T_l ^ T_{l+1} the planes where the threshold
+// bit flips (T_0 = T_9 = 0): 2 LOP3 per level and group instead of a compare
+// per step.  After kMcLevels levels an open step (probability 2^-kMcLevels)
+// takes the group's next tie word x and goes up iff
+// x < (thr_t << kMcLevels) mod 2^32.  5 Philox blocks per draw instead of
+// one word per step (13 blocks at 52 steps).
 //
 // Tie words: the k-th open step of group g (ascending) takes word
 // q = 2 k + g of the tie stream, word q % 4 of block kMcTieBlock0 + q / 4,
@@ -177,7 +188,7 @@ __device__ __forceinline__ void draw_bits(const McArgs& a, uint32_t (&B)[NS][2],
   for (int g = 0; g < 2; ++g) {
 #pragma unroll
     for (int d = 0; d < NS; ++d) {
-      B[d][g] = a.forced[g];
+      B[d][g] = a.bits0[g];
       U[d][g] = a.open[g];
     }
     if (32 * g < nsuf) {
@@ -189,12 +200,11 @@ __device__ __forceinline__ void draw_bits(const McArgs& a, uint32_t (&B)[NS][2],
           philox4x32_10(g * kMcPlaneBlocks + jb, i0 + d * stride, stream, rep, a.key0, a.key1, blk[d]);
 #pragma unroll
         for (int l = 0; l < 4; ++l) {
-          const uint32_t T = a.tmask[g][4 * jb + l];
+          const uint32_t C = a.flip[g][4 * jb + l];
 #pragma unroll
           for (int d = 0; d < NS; ++d) {
-            const uint32_t W = blk[d][l];
-            B[d][g] |= U[d][g] & ~W & T;
-            U[d][g] &= ~(W ^ T);
+            U[d][g] &= ~blk[d][l];
+            B[d][g] ^= U[d][g] & C;
           }
         }
       }
@@ -217,34 +227,50 @@ __device__ __forceinline__ void draw_bits(const McArgs& a, uint32_t (&B)[NS][2],
 // independent work).  Full blocks of 4 steps use the nibble tables; the
 // tail walks step by step.
 template <unsigned KIND, bool CONSTP, int NS>
-__device__ __forceinline__ void walk_suffix_n(const McArgs& a, const Nib* __restrict__ nib, PathState (&s)[NS],
-                                              uint32_t i0, uint32_t stride, uint32_t stream, uint32_t rep) {
+__device__ __forceinline__ void walk_suffix_n(const McArgs& a, const McTables& tab, PathState (&s)[NS], uint32_t i0,
+                                              uint32_t stride, uint32_t stream, uint32_t rep) {
   constexpr bool need_max = KIND == kFL;
   constexpr bool need_min = KIND == kFLP;
   constexpr bool need_sum = KIND == kAC || KIND == kAP;
   const int nsuf = a.N - a.r;
-  const int nfull = nsuf >> 2;
+  const int nbytes = nsuf >> 3;
   uint32_t B[NS][2];
   draw_bits<CONSTP, NS>(a, B, i0, stride, stream, rep);
+  auto advance = [&](PathState& st, double e, double c, double x, double n) {
+    if (need_sum) st.sum = fma(st.S, c, st.sum);
+    if (need_max) st.mx = fmax(st.mx, st.S * x);
+    if (need_min) st.mn = fmin(st.mn, st.S * n);
+    st.S *= e;
+  };
+  // whole bytes of 8 steps: one table entry each
 #pragma unroll
   for (int g = 0; g < 2; ++g) {
 #pragma unroll
-    for (int jj = 0; jj < 8; ++jj) {
-      if (8 * g + jj < nfull) {
+    for (int k = 0; k < 4; ++k) {
+      if (4 * g + k < nbytes) {
 #pragma unroll
         for (int d = 0; d < NS; ++d) {
-          // byte offset of entry (B >> 4 jj) & 15 in the 32-byte-entry table
-          const uint32_t off = (4 * jj >= 5 ? B[d][g] >> (4 * jj - 5) : B[d][g] << (5 - 4 * jj)) & 0x1E0u;
-          const Nib* q = reinterpret_cast<const Nib*>(reinterpret_cast<const char*>(nib) + off);
-          if (need_sum) s[d].sum = fma(s[d].S, q->c, s[d].sum);
-          if (need_max) s[d].mx = fmax(s[d].mx, s[d].S * q->x);
-          if (need_min) s[d].mn = fmin(s[d].mn, s[d].S * q->n);
-          s[d].S *= q->e;
+          // byte offset of entry (B >> 8 k) & 255 (one shift, one mask)
+          const uint32_t off = (k == 0 ? B[d][g] << 4 : B[d][g] >> (8 * k - 4)) & 0xFF0u;
+          const double2 ec = *reinterpret_cast<const double2*>(reinterpret_cast<const char*>(tab.ec) + off);
+          double2 xn = make_double2(0.0, 0.0);
+          if (need_max || need_min) xn = *reinterpret_cast<const double2*>(reinterpret_cast<const char*>(tab.xn) + off);
+          advance(s[d], ec.x, ec.y, xn.x, xn.y);
         }
       }
     }
   }
-  for (int w = 4 * nfull; w < nsuf; ++w) {
+  // a leftover nibble, then up to 3 single steps
+  int w = 8 * nbytes;
+  if (nsuf - w >= 4) {
+#pragma unroll
+    for (int d = 0; d < NS; ++d) {
+      const Nib q = tab.nib[(((w >> 5) ? B[d][1] : B[d][0]) >> (w & 31)) & 15u];
+      advance(s[d], q.e, q.c, q.x, q.n);
+    }
+    w += 4;
+  }
+  for (; w < nsuf; ++w) {
 #pragma unroll
     for (int d = 0; d < NS; ++d) {
       const uint32_t word = (w >> 5) ? B[d][1] : B[d][0];
@@ -257,10 +283,10 @@ __device__ __forceinline__ void walk_suffix_n(const McArgs& a, const Nib* __rest
 }
 
 template <unsigned KIND, bool CONSTP>
-__device__ __forceinline__ PathState walk_suffix(const McArgs& a, const Nib* __restrict__ nib, PathState st, uint32_t i,
+__device__ __forceinline__ PathState walk_suffix(const McArgs& a, const McTables& tab, PathState st, uint32_t i,
                                                  uint32_t stream, uint32_t rep) {
   PathState s[1] = {st};
-  walk_suffix_n<KIND, CONSTP, 1>(a, nib, s, i, 0u, stream, rep);
+  walk_suffix_n<KIND, CONSTP, 1>(a, tab, s, i, 0u, stream, rep);
   return s[0];
 }
 
@@ -298,8 +324,8 @@ __global__ void __launch_bounds__(kMcThreads, BP_MC_MINB)
 k_mc_strata(const __grid_constant__ McArgs a, const unsigned long long* __restrict__ draws,
             const unsigned long long* __restrict__ item_stratum, const unsigned long long* __restrict__ item_first,
             unsigned long long items_per_rep, int n_reps, double* __restrict__ item_out) {
-  __shared__ Nib nib[16];
-  build_nib(a, nib);
+  __shared__ __align__(16) McTables tab;
+  build_tables(a, tab);
   __syncthreads();
   const unsigned long long n_items = items_per_rep * (unsigned long long)n_reps;
   for (unsigned long long it = blockIdx.x; it < n_items; it += gridDim.x) {
@@ -318,18 +344,18 @@ k_mc_strata(const __grid_constant__ McArgs a, const unsigned long long* __restri
       PathState sd[kMcNS];
 #pragma unroll
       for (int d = 0; d < kMcNS; ++d) sd[d] = pre;
-      walk_suffix_n<KIND, CONSTP, kMcNS>(a, nib, sd, (uint32_t)i, kMcThreads, (uint32_t)m, a.rep0 + (uint32_t)k);
+      walk_suffix_n<KIND, CONSTP, kMcNS>(a, tab, sd, (uint32_t)i, kMcThreads, (uint32_t)m, a.rep0 + (uint32_t)k);
 #pragma unroll
       for (int d = 0; d < kMcNS; ++d) acc.add(payoff_of(KIND, sd[d], a.K, a.invN));
     }
     for (; kMcNS > 2 && i + kMcThreads < last; i += 2 * kMcThreads) {
       PathState sd[2] = {pre, pre};
-      walk_suffix_n<KIND, CONSTP, 2>(a, nib, sd, (uint32_t)i, kMcThreads, (uint32_t)m, a.rep0 + (uint32_t)k);
+      walk_suffix_n<KIND, CONSTP, 2>(a, tab, sd, (uint32_t)i, kMcThreads, (uint32_t)m, a.rep0 + (uint32_t)k);
       acc.add(payoff_of(KIND, sd[0], a.K, a.invN));
       acc.add(payoff_of(KIND, sd[1], a.K, a.invN));
     }
     if (i < last) {
-      const PathState st = walk_suffix<KIND, CONSTP>(a, nib, pre, (uint32_t)i, (uint32_t)m, a.rep0 + (uint32_t)k);
+      const PathState st = walk_suffix<KIND, CONSTP>(a, tab, pre, (uint32_t)i, (uint32_t)m, a.rep0 + (uint32_t)k);
       acc.add(payoff_of(KIND, st, a.K, a.invN));
     }
     const Welford t = cta_merge(acc.welford());
@@ -407,8 +433,8 @@ k_mc_shared(const __grid_constant__ McArgs a, unsigned long long R, const double
             const double* __restrict__ pre_tab /* [M][4] S, sum, mx, mn after r steps */, int M,
             unsigned long long items_per_rep, int n_reps, double* __restrict__ item_out,
             double* __restrict__ warp_sums /* [item][8][M] */) {
-  __shared__ Nib nib[16];
-  build_nib(a, nib);
+  __shared__ __align__(16) McTables tab;
+  build_tables(a, tab);
   __syncthreads();
   const unsigned long long n_items = items_per_rep * (unsigned long long)n_reps;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -426,7 +452,7 @@ k_mc_shared(const __grid_constant__ McArgs a, unsigned long long R, const double
       const bool live = i < last;
       // suffix relative to a unit start price
       PathState rel{1.0, 0.0, -INFINITY, INFINITY};
-      if (live) rel = walk_suffix<KIND, false>(a, nib, rel, (uint32_t)i, 0u, a.rep0 + (uint32_t)k);
+      if (live) rel = walk_suffix<KIND, false>(a, tab, rel, (uint32_t)i, 0u, a.rep0 + (uint32_t)k);
       double inner = 0.0;
       for (int m = 0; m < M; ++m) {
         const double S = pre_tab[4 * m], sum = pre_tab[4 * m + 1], mx = pre_tab[4 * m + 2], mn = pre_tab[4 * m + 3];

@@ -112,11 +112,10 @@ class PhiloxStream:
     def bits(self, probs: np.ndarray) -> np.ndarray:
         """Next draw's Bernoulli bits, bit t up with probability probs[t]
         (floor(p 2^32) / 2^32), by the engine's sampler with no fixed prefix:
-        step w is bit w % 32 of group w // 32; its 8 level bits (word
-        8 g + l, l = 0 first) against the top 8 bits of the threshold decide
-        it unless they are equal, then the group's next tie word (the k-th
-        tie of group g: word 16 + 2 k + g) does against the threshold's low
-        24 bits."""
+        step w is bit w % 32 of group w // 32; the first of its 8 level bits
+        (word 8 g + l) that is 1 decides it (up iff threshold bit 31 - l is
+        1); with no 1 the group's next tie word (the k-th tie of group g:
+        word 16 + 2 k + g) does against the threshold's low 24 bits."""
         probs = np.asarray(probs, dtype=np.float64)
         n = probs.shape[0]
         if n > 64:
@@ -133,12 +132,9 @@ class PhiloxStream:
                 continue
             thr = int(math.floor(min(max(p, 0.0), 1.0) * 4294967296.0))
             g, b = divmod(w, 32)
-            s = 0
-            for lvl in range(L):
-                s = (s << 1) | ((planes[L * g + lvl] >> b) & 1)
-            top = thr >> (32 - L)
-            if s != top:
-                up[w] = s < top
+            first = next((lvl for lvl in range(L) if (planes[L * g + lvl] >> b) & 1), None)
+            if first is not None:
+                up[w] = bool((thr >> (31 - first)) & 1)
                 continue
             q = 2 * L + 2 * ties[g] + g
             x = int(self.words(draw, q + 1)[q])
