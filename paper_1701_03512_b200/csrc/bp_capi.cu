@@ -1613,6 +1613,7 @@ static void fill_mc_args(const bp_tree* t, unsigned kind, int r, uint64_t seed, 
   a.kind = kind;
   a.key0 = (uint32_t)(seed & 0xffffffffull);
   a.key1 = (uint32_t)(seed >> 32);
+  philox_round_keys(a.key0, a.key1, a.rk);
   a.rep0 = rep0;
   for (int i = 0; i < t->n_steps; ++i) {
     const double p = t->up_probs[i];

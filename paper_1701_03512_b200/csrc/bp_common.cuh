@@ -96,4 +96,26 @@ BP_HD void philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3,
   out[3] = c3;
 }
 
+// The same block with the 10 round keys precomputed (rk[2 r], rk[2 r + 1];
+// philox_round_keys on the host): the MC kernels read them straight from the
+// parameter bank instead of running the key schedule once per block.
+BP_HD void philox_round_keys(uint32_t k0, uint32_t k1, uint32_t rk[20]) {
+  for (int r = 0; r < 10; ++r) {
+    rk[2 * r] = k0;
+    rk[2 * r + 1] = k1;
+    k0 += kPhiloxW0;
+    k1 += kPhiloxW1;
+  }
+}
+
+BP_HD void philox4x32_10_rk(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, const uint32_t (&rk)[20],
+                            uint32_t out[4]) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) philox_round(c0, c1, c2, c3, rk[2 * r], rk[2 * r + 1]);
+  out[0] = c0;
+  out[1] = c1;
+  out[2] = c2;
+  out[3] = c3;
+}
+
 }  // namespace bp

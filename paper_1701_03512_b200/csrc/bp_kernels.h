@@ -57,6 +57,7 @@ struct McArgs {
   int N, r;
   unsigned kind;
   uint32_t key0, key1;
+  uint32_t rk[20];  // Philox round keys of (key0, key1)
   uint32_t rep0;
 };
 cudaError_t launch_mc_strata(const McArgs& a, const unsigned long long* draws_dev,

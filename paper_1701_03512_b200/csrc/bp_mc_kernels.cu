@@ -115,6 +115,14 @@ struct McTables {
   Nib nib[16];
 };
 
+// shared-window address of p, opaque to the compiler so it stays in one
+// register instead of being rebuilt (S2UR + ULEA) before every table load
+__device__ __forceinline__ uint32_t shared_address(const void* p) {
+  uint32_t s = (uint32_t)__cvta_generic_to_shared(p);
+  asm volatile("" : "+r"(s));
+  return s;
+}
+
 __device__ __forceinline__ void build_tables(const McArgs& a, McTables& t) {
   for (int b = threadIdx.x; b < 256; b += blockDim.x) {
     double r = 1.0, c = 0.0, x = -INFINITY, n = INFINITY;
@@ -160,19 +168,19 @@ __device__ __forceinline__ void resolve_ties(const McArgs& a, uint32_t& Bg, uint
     if (CONSTP) return thr_tie;
     return a.thr[a.r + 32 * G + (__ffs((int)low) - 1)] << kMcLevels;
   };
+  const uint32_t first = u & (0u - u);
   if (CONSTP) {
-    if (tie[G] < thr_tie) Bg |= u & (0u - u);
+    if (tie[G] < thr_tie) Bg |= first;
   } else if (u) {
-    const uint32_t low = u & (0u - u);
-    if (tie[G] < tie_thr(low)) Bg |= low;
+    if (tie[G] < tie_thr(first)) Bg |= first;
   }
-  u &= u - 1u;
-  if (u == 0u) return;
+  if (u == first) return;
+  u ^= first;
   // second and later ties of the group (about 1 draw in 150)
   uint32_t blk[4] = {tie[0], tie[1], tie[2], tie[3]};
   for (uint32_t k = 1; u; ++k, u &= u - 1u) {
     const uint32_t q = 2u * k + G;
-    if ((q & 3u) == (uint32_t)G) philox4x32_10(kMcTieBlock0 + (q >> 2), draw, stream, rep, a.key0, a.key1, blk);
+    if ((q & 3u) == (uint32_t)G) philox4x32_10_rk(kMcTieBlock0 + (q >> 2), draw, stream, rep, a.rk, blk);
     const uint32_t x = (q & 2u) ? blk[2 + G] : blk[G];
     const uint32_t low = u & (0u - u);
     if (x < tie_thr(low)) Bg |= low;
@@ -197,7 +205,7 @@ __device__ __forceinline__ void draw_bits(const McArgs& a, uint32_t (&B)[NS][2],
         uint32_t blk[NS][4];
 #pragma unroll
         for (int d = 0; d < NS; ++d)
-          philox4x32_10(g * kMcPlaneBlocks + jb, i0 + d * stride, stream, rep, a.key0, a.key1, blk[d]);
+          philox4x32_10_rk(g * kMcPlaneBlocks + jb, i0 + d * stride, stream, rep, a.rk, blk[d]);
 #pragma unroll
         for (int l = 0; l < 4; ++l) {
           const uint32_t C = a.flip[g][4 * jb + l];
@@ -214,7 +222,7 @@ __device__ __forceinline__ void draw_bits(const McArgs& a, uint32_t (&B)[NS][2],
   uint32_t tie[NS][4];
 #pragma unroll
   for (int d = 0; d < NS; ++d)
-    philox4x32_10(kMcTieBlock0, i0 + d * stride, stream, rep, a.key0, a.key1, tie[d]);
+    philox4x32_10_rk(kMcTieBlock0, i0 + d * stride, stream, rep, a.rk, tie[d]);
 #pragma unroll
   for (int d = 0; d < NS; ++d) {
     resolve_ties<CONSTP, 0>(a, B[d][0], U[d][0], tie[d], thr_tie, i0 + d * stride, stream, rep);
@@ -227,8 +235,8 @@ __device__ __forceinline__ void draw_bits(const McArgs& a, uint32_t (&B)[NS][2],
 // independent work).  Full blocks of 4 steps use the nibble tables; the
 // tail walks step by step.
 template <unsigned KIND, bool CONSTP, int NS>
-__device__ __forceinline__ void walk_suffix_n(const McArgs& a, const McTables& tab, PathState (&s)[NS], uint32_t i0,
-                                              uint32_t stride, uint32_t stream, uint32_t rep) {
+__device__ __forceinline__ void walk_suffix_n(const McArgs& a, const McTables& tab, uint32_t tab_s, PathState (&s)[NS],
+                                              uint32_t i0, uint32_t stride, uint32_t stream, uint32_t rep) {
   constexpr bool need_max = KIND == kFL;
   constexpr bool need_min = KIND == kFLP;
   constexpr bool need_sum = KIND == kAC || KIND == kAP;
@@ -242,7 +250,9 @@ __device__ __forceinline__ void walk_suffix_n(const McArgs& a, const McTables& t
     if (need_min) st.mn = fmin(st.mn, st.S * n);
     st.S *= e;
   };
-  // whole bytes of 8 steps: one table entry each
+  // whole bytes of 8 steps, one table entry each: entry address = table
+  // base + 16 x byte (PRMT + LEA; tab_s is the table's shared-window address,
+  // made once per kernel)
 #pragma unroll
   for (int g = 0; g < 2; ++g) {
 #pragma unroll
@@ -250,12 +260,11 @@ __device__ __forceinline__ void walk_suffix_n(const McArgs& a, const McTables& t
       if (4 * g + k < nbytes) {
 #pragma unroll
         for (int d = 0; d < NS; ++d) {
-          // byte offset of entry (B >> 8 k) & 255 (one shift, one mask)
-          const uint32_t off = (k == 0 ? B[d][g] << 4 : B[d][g] >> (8 * k - 4)) & 0xFF0u;
-          const double2 ec = *reinterpret_cast<const double2*>(reinterpret_cast<const char*>(tab.ec) + off);
-          double2 xn = make_double2(0.0, 0.0);
-          if (need_max || need_min) xn = *reinterpret_cast<const double2*>(reinterpret_cast<const char*>(tab.xn) + off);
-          advance(s[d], ec.x, ec.y, xn.x, xn.y);
+          const uint32_t addr = tab_s + (__byte_perm(B[d][g], 0u, 0x4440u + k) << 4);
+          double e, c, x = 0.0, n = 0.0;
+          asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(e), "=d"(c) : "r"(addr));
+          if (need_max || need_min) asm("ld.shared.v2.f64 {%0, %1}, [%2+4096];" : "=d"(x), "=d"(n) : "r"(addr));
+          advance(s[d], e, c, x, n);
         }
       }
     }
@@ -283,10 +292,10 @@ __device__ __forceinline__ void walk_suffix_n(const McArgs& a, const McTables& t
 }
 
 template <unsigned KIND, bool CONSTP>
-__device__ __forceinline__ PathState walk_suffix(const McArgs& a, const McTables& tab, PathState st, uint32_t i,
+__device__ __forceinline__ PathState walk_suffix(const McArgs& a, const McTables& tab, uint32_t tab_s, PathState st, uint32_t i,
                                                  uint32_t stream, uint32_t rep) {
   PathState s[1] = {st};
-  walk_suffix_n<KIND, CONSTP, 1>(a, tab, s, i, 0u, stream, rep);
+  walk_suffix_n<KIND, CONSTP, 1>(a, tab, tab_s, s, i, 0u, stream, rep);
   return s[0];
 }
 
@@ -326,6 +335,7 @@ k_mc_strata(const __grid_constant__ McArgs a, const unsigned long long* __restri
             unsigned long long items_per_rep, int n_reps, double* __restrict__ item_out) {
   __shared__ __align__(16) McTables tab;
   build_tables(a, tab);
+  const uint32_t tab_s = shared_address(&tab);
   __syncthreads();
   const unsigned long long n_items = items_per_rep * (unsigned long long)n_reps;
   for (unsigned long long it = blockIdx.x; it < n_items; it += gridDim.x) {
@@ -344,18 +354,18 @@ k_mc_strata(const __grid_constant__ McArgs a, const unsigned long long* __restri
       PathState sd[kMcNS];
 #pragma unroll
       for (int d = 0; d < kMcNS; ++d) sd[d] = pre;
-      walk_suffix_n<KIND, CONSTP, kMcNS>(a, tab, sd, (uint32_t)i, kMcThreads, (uint32_t)m, a.rep0 + (uint32_t)k);
+      walk_suffix_n<KIND, CONSTP, kMcNS>(a, tab, tab_s, sd, (uint32_t)i, kMcThreads, (uint32_t)m, a.rep0 + (uint32_t)k);
 #pragma unroll
       for (int d = 0; d < kMcNS; ++d) acc.add(payoff_of(KIND, sd[d], a.K, a.invN));
     }
     for (; kMcNS > 2 && i + kMcThreads < last; i += 2 * kMcThreads) {
       PathState sd[2] = {pre, pre};
-      walk_suffix_n<KIND, CONSTP, 2>(a, tab, sd, (uint32_t)i, kMcThreads, (uint32_t)m, a.rep0 + (uint32_t)k);
+      walk_suffix_n<KIND, CONSTP, 2>(a, tab, tab_s, sd, (uint32_t)i, kMcThreads, (uint32_t)m, a.rep0 + (uint32_t)k);
       acc.add(payoff_of(KIND, sd[0], a.K, a.invN));
       acc.add(payoff_of(KIND, sd[1], a.K, a.invN));
     }
     if (i < last) {
-      const PathState st = walk_suffix<KIND, CONSTP>(a, tab, pre, (uint32_t)i, (uint32_t)m, a.rep0 + (uint32_t)k);
+      const PathState st = walk_suffix<KIND, CONSTP>(a, tab, tab_s, pre, (uint32_t)i, (uint32_t)m, a.rep0 + (uint32_t)k);
       acc.add(payoff_of(KIND, st, a.K, a.invN));
     }
     const Welford t = cta_merge(acc.welford());
@@ -435,6 +445,7 @@ k_mc_shared(const __grid_constant__ McArgs a, unsigned long long R, const double
             double* __restrict__ warp_sums /* [item][8][M] */) {
   __shared__ __align__(16) McTables tab;
   build_tables(a, tab);
+  const uint32_t tab_s = shared_address(&tab);
   __syncthreads();
   const unsigned long long n_items = items_per_rep * (unsigned long long)n_reps;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -452,7 +463,7 @@ k_mc_shared(const __grid_constant__ McArgs a, unsigned long long R, const double
       const bool live = i < last;
       // suffix relative to a unit start price
       PathState rel{1.0, 0.0, -INFINITY, INFINITY};
-      if (live) rel = walk_suffix<KIND, false>(a, tab, rel, (uint32_t)i, 0u, a.rep0 + (uint32_t)k);
+      if (live) rel = walk_suffix<KIND, false>(a, tab, tab_s, rel, (uint32_t)i, 0u, a.rep0 + (uint32_t)k);
       double inner = 0.0;
       for (int m = 0; m < M; ++m) {
         const double S = pre_tab[4 * m], sum = pre_tab[4 * m + 1], mx = pre_tab[4 * m + 2], mn = pre_tab[4 * m + 3];
