@@ -14,10 +14,13 @@
 //   first level whose bit is 1 decides the step: up iff bit (31 - l) of
 //   thr_t = floor(p_t 2^32) is 1 (level l is first with probability
 //   2^-(l+1), so P(up) so far is the top 8 bits of thr_t).  A step with no 1
-//   in 8 levels (probability 2^-8) takes its group's next tie word x (the
-//   k-th such step of group g in ascending order: word q = 2 k + g of the tie
-//   stream, i.e. word q % 4 of block 4 + q / 4) and goes up iff
-//   x < (thr_t << 8) mod 2^32.  P(up) = thr_t / 2^32 exactly; p_t == 1: always.
+//   in 8 levels (probability 2^-8) takes its group's next tie word x and goes
+//   up iff x < (thr_t << 8) mod 2^32.  P(up) = thr_t / 2^32 exactly; p_t == 1:
+//   always.  Tie words: draws 2 j and 2 j + 1 share the pair block with
+//   counter (4, j, m, rep); the first tie of group g of draw i (ascending step
+//   order) takes its word 2 (i mod 2) + g.  Later ties of the group (the
+//   k-th, k >= 1) take word q = 2 (k - 1) + g of the draw's own overflow
+//   stream: word q % 4 of block (5 + q / 4, i, m, rep).
 // Streams are disjoint by construction and independent of the thread
 // mapping, so results do not depend on the grid, the GPU count or timing.
 //
@@ -155,41 +158,43 @@ constexpr uint32_t kMcTieBlock0 = 2 * kMcPlaneBlocks;  // first block of the tie
 // x < (thr_t << kMcLevels) mod 2^32.  5 Philox blocks per draw instead of
 // one word per step (13 blocks at 52 steps).
 //
-// Tie words: the k-th open step of group g (ascending) takes word
-// q = 2 k + g of the tie stream, word q % 4 of block kMcTieBlock0 + q / 4,
-// so each group's first two ties are served by the one block every draw
-// computes.  CONSTP (every suffix step has the same threshold): the first
-// tie of a group needs no bit search -- the lowest open bit u & -u goes up
-// iff its word is below the common tie threshold.
+// Tie words: draws 2 j and 2 j + 1 share one pair block (4 words: 2 draws x
+// 2 groups) for the first tie of each group, so a thread walking the two
+// draws of a pair in lock step computes 4 + 1/2 Philox blocks per draw.
+// CONSTP (every suffix step has the same threshold): the first tie of a
+// group needs no bit search -- the lowest open bit u & -u goes up iff its
+// word is below the common tie threshold.  Second and later ties of a group
+// (about 1 draw in 150) take words of the draw's own overflow blocks.
 template <bool CONSTP, int G>
-__device__ __forceinline__ void resolve_ties(const McArgs& a, uint32_t& Bg, uint32_t u, const uint32_t (&tie)[4],
-                                             uint32_t thr_tie, uint32_t draw, uint32_t stream, uint32_t rep) {
+__device__ __forceinline__ void resolve_ties(const McArgs& a, uint32_t& Bg, uint32_t u, uint32_t x0, uint32_t thr_tie,
+                                             uint32_t draw, uint32_t stream, uint32_t rep) {
   auto tie_thr = [&](uint32_t low) -> uint32_t {
     if (CONSTP) return thr_tie;
     return a.thr[a.r + 32 * G + (__ffs((int)low) - 1)] << kMcLevels;
   };
   const uint32_t first = u & (0u - u);
   if (CONSTP) {
-    if (tie[G] < thr_tie) Bg |= first;
+    if (x0 < thr_tie) Bg |= first;
   } else if (u) {
-    if (tie[G] < tie_thr(first)) Bg |= first;
+    if (x0 < tie_thr(first)) Bg |= first;
   }
   if (u == first) return;
   u ^= first;
-  // second and later ties of the group (about 1 draw in 150)
-  uint32_t blk[4] = {tie[0], tie[1], tie[2], tie[3]};
+  uint32_t blk[4] = {0u, 0u, 0u, 0u};
   for (uint32_t k = 1; u; ++k, u &= u - 1u) {
-    const uint32_t q = 2u * k + G;
-    if ((q & 3u) == (uint32_t)G) philox4x32_10_rk(kMcTieBlock0 + (q >> 2), draw, stream, rep, a.rk, blk);
+    const uint32_t q = 2u * (k - 1u) + G;
+    if ((q & 3u) == (uint32_t)G) philox4x32_10_rk(kMcTieBlock0 + 1u + (q >> 2), draw, stream, rep, a.rk, blk);
     const uint32_t x = (q & 2u) ? blk[2 + G] : blk[G];
     const uint32_t low = u & (0u - u);
     if (x < tie_thr(low)) Bg |= low;
   }
 }
 
+// NS == 1: any draw i0.  NS even: the consecutive draws i0 .. i0 + NS - 1, i0 even.
 template <bool CONSTP, int NS>
-__device__ __forceinline__ void draw_bits(const McArgs& a, uint32_t (&B)[NS][2], uint32_t i0, uint32_t stride,
-                                          uint32_t stream, uint32_t rep) {
+__device__ __forceinline__ void draw_bits(const McArgs& a, uint32_t (&B)[NS][2], uint32_t i0, uint32_t stream,
+                                          uint32_t rep) {
+  static_assert(NS == 1 || NS % 2 == 0, "draws are walked singly or in whole pairs");
   const int nsuf = a.N - a.r;
   uint32_t U[NS][2];
 #pragma unroll
@@ -204,8 +209,7 @@ __device__ __forceinline__ void draw_bits(const McArgs& a, uint32_t (&B)[NS][2],
       for (int jb = 0; jb < (int)kMcPlaneBlocks; ++jb) {
         uint32_t blk[NS][4];
 #pragma unroll
-        for (int d = 0; d < NS; ++d)
-          philox4x32_10_rk(g * kMcPlaneBlocks + jb, i0 + d * stride, stream, rep, a.rk, blk[d]);
+        for (int d = 0; d < NS; ++d) philox4x32_10_rk(g * kMcPlaneBlocks + jb, i0 + d, stream, rep, a.rk, blk[d]);
 #pragma unroll
         for (int l = 0; l < 4; ++l) {
           const uint32_t C = a.flip[g][4 * jb + l];
@@ -219,31 +223,39 @@ __device__ __forceinline__ void draw_bits(const McArgs& a, uint32_t (&B)[NS][2],
     }
   }
   const uint32_t thr_tie = a.thr[a.r < a.N ? a.r : 0] << kMcLevels;
-  uint32_t tie[NS][4];
+  constexpr int NP = NS == 1 ? 1 : NS / 2;
+  uint32_t tie[NP][4];
 #pragma unroll
-  for (int d = 0; d < NS; ++d)
-    philox4x32_10_rk(kMcTieBlock0, i0 + d * stride, stream, rep, a.rk, tie[d]);
+  for (int pr = 0; pr < NP; ++pr) philox4x32_10_rk(kMcTieBlock0, (i0 >> 1) + pr, stream, rep, a.rk, tie[pr]);
 #pragma unroll
   for (int d = 0; d < NS; ++d) {
-    resolve_ties<CONSTP, 0>(a, B[d][0], U[d][0], tie[d], thr_tie, i0 + d * stride, stream, rep);
-    resolve_ties<CONSTP, 1>(a, B[d][1], U[d][1], tie[d], thr_tie, i0 + d * stride, stream, rep);
+    uint32_t x0, x1;
+    if (NS == 1) {
+      x0 = (i0 & 1u) ? tie[0][2] : tie[0][0];
+      x1 = (i0 & 1u) ? tie[0][3] : tie[0][1];
+    } else {
+      x0 = tie[d / 2][2 * (d & 1)];
+      x1 = tie[d / 2][2 * (d & 1) + 1];
+    }
+    resolve_ties<CONSTP, 0>(a, B[d][0], U[d][0], x0, thr_tie, i0 + d, stream, rep);
+    resolve_ties<CONSTP, 1>(a, B[d][1], U[d][1], x1, thr_tie, i0 + d, stream, rep);
   }
 }
 
-// Walk the N - r suffix steps of NS draws in lock step from their states
-// (the Philox rounds of the NS counters interleave, giving the scheduler
-// independent work).  Full blocks of 4 steps use the nibble tables; the
+// Walk the N - r suffix steps of NS draws (draw_bits: one draw, or whole
+// pairs) in lock step from their states (the Philox rounds of the NS
+// counters interleave, giving the scheduler independent work).  Full blocks of 4 steps use the nibble tables; the
 // tail walks step by step.
 template <unsigned KIND, bool CONSTP, int NS>
 __device__ __forceinline__ void walk_suffix_n(const McArgs& a, const McTables& tab, uint32_t tab_s, PathState (&s)[NS],
-                                              uint32_t i0, uint32_t stride, uint32_t stream, uint32_t rep) {
+                                              uint32_t i0, uint32_t stream, uint32_t rep) {
   constexpr bool need_max = KIND == kFL;
   constexpr bool need_min = KIND == kFLP;
   constexpr bool need_sum = KIND == kAC || KIND == kAP;
   const int nsuf = a.N - a.r;
   const int nbytes = nsuf >> 3;
   uint32_t B[NS][2];
-  draw_bits<CONSTP, NS>(a, B, i0, stride, stream, rep);
+  draw_bits<CONSTP, NS>(a, B, i0, stream, rep);
   auto advance = [&](PathState& st, double e, double c, double x, double n) {
     if (need_sum) st.sum = fma(st.S, c, st.sum);
     if (need_max) st.mx = fmax(st.mx, st.S * x);
@@ -295,12 +307,12 @@ template <unsigned KIND, bool CONSTP>
 __device__ __forceinline__ PathState walk_suffix(const McArgs& a, const McTables& tab, uint32_t tab_s, PathState st, uint32_t i,
                                                  uint32_t stream, uint32_t rep) {
   PathState s[1] = {st};
-  walk_suffix_n<KIND, CONSTP, 1>(a, tab, tab_s, s, i, 0u, stream, rep);
+  walk_suffix_n<KIND, CONSTP, 1>(a, tab, tab_s, s, i, stream, rep);
   return s[0];
 }
 
 #ifndef BP_MC_NS
-#define BP_MC_NS 2  // draws per thread in lock step (K4; r2 scan: 2, 4, 8 within 1 %)
+#define BP_MC_NS 2  // draws per thread in lock step (K4; even: whole pairs; r2 scan: 2 and 4 within 1 %)
 #endif
 constexpr int kMcNS = BP_MC_NS;
 
@@ -346,25 +358,24 @@ k_mc_strata(const __grid_constant__ McArgs a, const unsigned long long* __restri
     const unsigned long long last = first + kChunk < R ? first + kChunk : R;
     const PathState pre = prefix_state(a, m);
     ShiftedSums acc{0.0, 0.0, 0.0, 0.0};
-    unsigned long long i = first + threadIdx.x;
-    // groups of kMcNS draws (i, i + 256, ...) in lock step, then pairs, then a
-    // possible single tail draw; values are added in ascending draw order, as
-    // the one-at-a-time loop did
-    for (; i + (kMcNS - 1) * kMcThreads < last; i += kMcNS * kMcThreads) {
-      PathState sd[kMcNS];
+    // whole pairs (2 j, 2 j + 1) in groups of kMcNS consecutive draws per
+    // thread, then the remaining draws one per thread; an item starting at an
+    // odd draw (bp_mc_range with an unaligned range) walks them all singly
+    unsigned long long single0 = first;
+    if ((first & 1ull) == 0ull) {
+      const unsigned long long span = (unsigned long long)kMcNS * kMcThreads;
+      const unsigned long long whole = (last - first) / span * span;
+      for (unsigned long long i = first + (unsigned long long)kMcNS * threadIdx.x; i < first + whole; i += span) {
+        PathState sd[kMcNS];
 #pragma unroll
-      for (int d = 0; d < kMcNS; ++d) sd[d] = pre;
-      walk_suffix_n<KIND, CONSTP, kMcNS>(a, tab, tab_s, sd, (uint32_t)i, kMcThreads, (uint32_t)m, a.rep0 + (uint32_t)k);
+        for (int d = 0; d < kMcNS; ++d) sd[d] = pre;
+        walk_suffix_n<KIND, CONSTP, kMcNS>(a, tab, tab_s, sd, (uint32_t)i, (uint32_t)m, a.rep0 + (uint32_t)k);
 #pragma unroll
-      for (int d = 0; d < kMcNS; ++d) acc.add(payoff_of(KIND, sd[d], a.K, a.invN));
+        for (int d = 0; d < kMcNS; ++d) acc.add(payoff_of(KIND, sd[d], a.K, a.invN));
+      }
+      single0 = first + whole;
     }
-    for (; kMcNS > 2 && i + kMcThreads < last; i += 2 * kMcThreads) {
-      PathState sd[2] = {pre, pre};
-      walk_suffix_n<KIND, CONSTP, 2>(a, tab, tab_s, sd, (uint32_t)i, kMcThreads, (uint32_t)m, a.rep0 + (uint32_t)k);
-      acc.add(payoff_of(KIND, sd[0], a.K, a.invN));
-      acc.add(payoff_of(KIND, sd[1], a.K, a.invN));
-    }
-    if (i < last) {
+    for (unsigned long long i = single0 + threadIdx.x; i < last; i += kMcThreads) {
       const PathState st = walk_suffix<KIND, CONSTP>(a, tab, tab_s, pre, (uint32_t)i, (uint32_t)m, a.rep0 + (uint32_t)k);
       acc.add(payoff_of(KIND, st, a.K, a.invN));
     }

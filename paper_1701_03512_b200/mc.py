@@ -96,6 +96,14 @@ class PhiloxStream:
         self.seed, self.stratum, self.rep = int(seed), int(stratum), int(rep)
         self._draw = 0
 
+    def _block(self, j: int, c1: int) -> list:
+        """Philox block with counter (j, c1, stratum, rep)."""
+        key = (ctypes.c_uint32 * 2)(self.seed & 0xFFFFFFFF, self.seed >> 32)
+        ctr = (ctypes.c_uint32 * 4)(j, c1, self.stratum, self.rep)
+        blk = (ctypes.c_uint32 * 4)()
+        _native.lib().bp_philox4x32_10(ctr, key, blk)
+        return list(blk)
+
     def words(self, draw: int, count: int) -> np.ndarray:
         key = (ctypes.c_uint32 * 2)(self.seed & 0xFFFFFFFF, self.seed >> 32)
         out = np.empty(count, dtype=np.uint32)
@@ -114,8 +122,10 @@ class PhiloxStream:
         (floor(p 2^32) / 2^32), by the engine's sampler with no fixed prefix:
         step w is bit w % 32 of group w // 32; the first of its 8 level bits
         (word 8 g + l) that is 1 decides it (up iff threshold bit 31 - l is
-        1); with no 1 the group's next tie word (the k-th tie of group g:
-        word 16 + 2 k + g) does against the threshold's low 24 bits."""
+        1); with no 1 the group's next tie word does against the threshold's
+        low 24 bits: the first tie of group g takes word 2 (i % 2) + g of the
+        block (4, i // 2) that draws 2 j and 2 j + 1 share, the k-th (k >= 1)
+        word 2 (k - 1) + g of the draw's own blocks 5, 6, ..."""
         probs = np.asarray(probs, dtype=np.float64)
         n = probs.shape[0]
         if n > 64:
@@ -136,8 +146,11 @@ class PhiloxStream:
             if first is not None:
                 up[w] = bool((thr >> (31 - first)) & 1)
                 continue
-            q = 2 * L + 2 * ties[g] + g
-            x = int(self.words(draw, q + 1)[q])
+            if ties[g] == 0:
+                x = int(self._block(2 * L // 4, draw >> 1)[2 * (draw & 1) + g])
+            else:
+                q = 2 * (ties[g] - 1) + g
+                x = int(self._block(2 * L // 4 + 1 + q // 4, draw)[q % 4])
             up[w] = x < ((thr << L) & 0xFFFFFFFF)
             ties[g] += 1
         return up

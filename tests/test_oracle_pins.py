@@ -110,18 +110,18 @@ def test_mc_oracle_single_stratum_equals_basic_and_is_unbiased():
 def test_sampler_host_view_matches_oracle_bits():
     """PhiloxStream.bits (host view of the engine's stream) and the oracle's
     step-by-step restatement of the sampler give the same bits, for steps in
-    both 32-step groups, forced steps (p = 1), p = 0 and thresholds whose top
-    byte ties often."""
+    both 32-step groups, forced steps (p = 1), p = 0, odd and even draws (the
+    two halves of a pair block) and enough draws for first and later ties."""
     import paper_1701_03512_b200 as bp
     rng = np.random.default_rng(5)
     for N in (1, 7, 32, 33, 52, 64):
         probs = rng.uniform(0.0, 1.0, N)
-        probs[::5] = 0.5 + 2.0 ** -20  # the top 8 bits tie with probability 2^-8
+        probs[::5] = 0.5 + 2.0 ** -20  # low threshold bits set: the tie words matter
         if N > 3:
             probs[1], probs[3] = 1.0, 0.0
         for stream, rep in ((0, 0), (11, 3)):
             host = bp.mc_stream(1234567890123, stream, rep)
-            for draw in range(40):
+            for draw in range(200):
                 want = oracle.mc_bits(N, 0, probs, 1234567890123, stream, rep, draw)
                 got = host.bits(probs)
                 assert np.array_equal(got, want), (N, stream, rep, draw)
