@@ -77,6 +77,18 @@ def test_range_matches_oracle_draw_for_draw():
     assert np.allclose(mean, om, rtol=1e-12, atol=1e-14) and np.allclose(m2, o2, rtol=1e-11, atol=1e-12)
 
 
+def test_unaligned_ranges_match_oracle_draw_for_draw():
+    """Ranges starting or ending at odd draws: a draw's tie words come from the
+    pair block it shares with its neighbour whether or not that neighbour is
+    in the range (an odd start walks the range draw by draw)."""
+    req = _req(N=40)
+    P = req.params
+    first, end = [4097, 1, 8191, 101], [4097 + 778, 50, 8191 + 4097, 4196]
+    mean, m2 = _range(req, 2, first, end, 3)
+    om, o2 = oracle.mc_range(40, 100.0, 100.0, P.u, P.d, P.up_probs[0], "asian-call", 2, first, end, 3)
+    assert np.allclose(mean, om, rtol=1e-12, atol=1e-14) and np.allclose(m2, o2, rtol=1e-11, atol=1e-12)
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))

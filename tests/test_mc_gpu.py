@@ -184,3 +184,26 @@ def test_sigma_zero_all_up_paths():
     est = bp.estimate_basic(req, bp.McConfig(R=64, seed=1))
     assert est.variance == 0.0
     assert est.value == pytest.approx(math.exp(-0.05) * (2.0 * params.u ** 8 - 1.0), rel=1e-13)
+
+
+def test_sampler_later_ties_match_oracle_at_depth():
+    """2^20 draws of 64 (62) stream-decided steps: about 7000 draws have a
+    second tie in a group and ~300 a third, so the pair block, the overflow
+    blocks and the per-step tie thresholds (general path) are all exercised;
+    one wrong bit in one draw would move theta by ~1e-7 relative."""
+    R = 1 << 20
+    req64 = classic_req(64)
+    P = req64.params
+    theta, sse, _ = bp.mc._strata_stats(req64, 0, [R], 17, 0, 1)
+    ot, os_ = oracle.mc_strata(64, 100.0, 100.0, P.u, P.d, P.up_probs, "asian-call", 0, [R], 17, 0, 1)
+    np.testing.assert_allclose(theta, ot, rtol=1e-12)
+    np.testing.assert_allclose(sse, os_, rtol=1e-9)
+    rng = np.random.default_rng(8)
+    inputs = bp.MarketInputs(S0=50.0, K=52.0, q=0.03, sigma=0.4, T=1.0, N=62)
+    params = bp.with_custom_probs(inputs, rng.uniform(0.05, 0.95, size=62))
+    req = bp.ValuationRequest(inputs=inputs, params=params, kind=bp.resolve_kind("float-lookback"), force_large=True)
+    theta, sse, _ = bp.mc._strata_stats(req, 0, [R // 4], 23, 2, 1)
+    ot, os_ = oracle.mc_strata(62, 50.0, 52.0, params.u, params.d, params.up_probs, "float-lookback", 0, [R // 4],
+                               23, 2, 1)
+    np.testing.assert_allclose(theta, ot, rtol=1e-12)
+    np.testing.assert_allclose(sse, os_, rtol=1e-9)
