@@ -477,7 +477,17 @@ def secondary_configs(dev):
                       "value": (R_m << k) / (t * 1e-3), "unit": "draws/s", "kernel_ms": t,
                       "estimate": e.value, "std_error": e.std_error, "basic_estimate": b.value,
                       "basic_std_error": b.std_error, "variance_ratio_basic_over_equal": b.variance / e.variance,
-                      "reference_ratio_N62": 1.60, "gpus": 1}
+                      "reference_ratio_N62": 1.60, "gpus": 1,
+                      "sampler": {"philox_blocks_per_draw": 4.5,
+                                  "philox_blocks_per_s": 4.5 * (R_m << k) / (t * 1e-3),
+                                  "philox_ceiling_blocks_per_s": 5.15e11,
+                                  "frac_of_philox_ceiling": 4.5 * (R_m << k) / (t * 1e-3) / 5.15e11,
+                                  "warp_inst_per_draw": 365.5,
+                                  "note": "bit-sliced sampler: 8 threshold bits decided 32 steps per Philox word, "
+                                          "tie words for the 2^-8 rest (exactly floor(p 2^32)/2^32 per step); "
+                                          "ceiling = Philox4x32-10 alone, tools/microbench/mb_philox.cu "
+                                          "(profiles/r1_microbench_philox.log); instruction count from "
+                                          "profiles/r2_config4_full.ncu-rep"}}
     n, Nb = 4096, 24
     rng = np.random.default_rng(0)
     S0 = rng.uniform(50, 150, n); m = rng.uniform(0.8, 1.2, n); K = m * S0
