@@ -48,10 +48,11 @@ __device__ inline void batch_group_prefix(const double* __restrict__ tab, double
   }
 }
 
-// next integer with the same number of set bits (Gosper's hack)
+// next integer with the same number of set bits (Gosper's hack; the division
+// by the lowest set bit c = v & -v is a shift by its position)
 __device__ __forceinline__ int next_same_popc(int v) {
   const int c = v & -v, r = v + c;
-  return (((r ^ v) >> 2) / c) | r;
+  return (int)((unsigned)(r ^ v) >> (1 + __ffs(v))) | r;
 }
 
 template <unsigned KIND>
