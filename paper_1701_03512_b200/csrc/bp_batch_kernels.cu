@@ -29,6 +29,24 @@ struct BatchArgs {
   BatchLayout lay;
 };
 
+// Class layout of the inner block for a RUNTIME class index: binom() and
+// class_start() are constexpr loops with 64-bit divisions; called with a
+// runtime argument they ran on the device (6 % of K3's instructions).  One
+// compile-time table instead.
+struct BatchClassTab {
+  int start[kBL + 2], size[kBL + 1];
+  bool screened[kBL + 1];
+  constexpr BatchClassTab() : start{}, size{}, screened{} {
+    for (int c = 0; c <= kBL; ++c) {
+      start[c] = class_start(kBL, c);
+      size[c] = binom(kBL, c);
+      screened[c] = i15_class(kBL, c);
+    }
+    start[kBL + 1] = 1 << kBL;
+  }
+};
+__constant__ BatchClassTab c_btab{};
+
 // group prefix sums of class C (compile-time layout: no runtime binomials)
 template <int C, bool SMALL_ONLY>
 __device__ inline void batch_group_prefix(const double* __restrict__ tab, double* __restrict__ gpre) {
@@ -130,7 +148,7 @@ k_exact_batch(const BatchOption* __restrict__ opts, BatchArgs ba, double2* __res
         const double v2 = tab[s2];
         rank += DESC ? (v2 > v[q] || (v2 == v[q] && s2 < sfx)) : (v2 < v[q] || (v2 == v[q] && s2 < sfx));
       }
-      pos[q] = class_start(kBL, cls) + rank;
+      pos[q] = c_btab.start[cls] + rank;
     }
   }
   __syncthreads();
@@ -160,7 +178,7 @@ k_exact_batch(const BatchOption* __restrict__ opts, BatchArgs ba, double2* __res
     for (int j = 0; j < tid; ++j) r *= o.u;
     for (int j = tid; j < kBL; ++j) r *= o.d;
     e_cls[tid] = r;
-    b_cls[tid] = (double)binom(kBL, tid);
+    b_cls[tid] = (double)c_btab.size[tid];
   }
   __syncthreads();
   // group prefix sums (compensated, rounded once), one (group, n) per thread;
@@ -184,8 +202,8 @@ k_exact_batch(const BatchOption* __restrict__ opts, BatchArgs ba, double2* __res
     gray_fill_small<kBL, 0>(reinterpret_cast<const double(*)[kGroupSlots]>(gpre), sgray);
     // per big class (one thread each): the monotone map onto [4, 32763] (as
     // the host builds it for K1, i15_layout) and the class prefix sums
-    if (tid < NC && i15_class(kBL, tid)) {
-      const int c = tid, i0 = class_start(kBL, c), len = binom(kBL, c);
+    if (tid < NC && c_btab.screened[tid]) {
+      const int c = tid, i0 = c_btab.start[c], len = c_btab.size[c];
       float lo = (float)tab[i0], hi = lo;
       for (int k = 0; k < len; ++k) {
         lo = fminf(lo, (float)tab[i0 + k]);
@@ -210,9 +228,9 @@ k_exact_batch(const BatchOption* __restrict__ opts, BatchArgs ba, double2* __res
     // per position: the screened value in both lanes and the tie-run end
     for (int i = tid; i < NL; i += kBThreads) {
       int c = 0;
-      while (i >= class_start(kBL, c + 1)) ++c;
-      if (i15_class(kBL, c)) {
-        const int i0 = class_start(kBL, c), len = binom(kBL, c);
+      while (i >= c_btab.start[c + 1]) ++c;
+      if (c_btab.screened[c]) {
+        const int i0 = c_btab.start[c], len = c_btab.size[c];
         const unsigned k = i15_map((float)tab[i], i15_s[c], i15_o[c]);
         i15_xq[i] = k | (k << 16);
         const double tol = ldexp(fabs(tab[i]), -44);
