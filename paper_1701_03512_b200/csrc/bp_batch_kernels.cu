@@ -36,13 +36,20 @@ struct BatchArgs {
 struct BatchClassTab {
   int start[kBL + 2], size[kBL + 1];
   bool screened[kBL + 1];
-  constexpr BatchClassTab() : start{}, size{}, screened{} {
+  unsigned short cm[1 << kBL];  // class-major position of leaf s (ascending s inside a class)
+  constexpr BatchClassTab() : start{}, size{}, screened{}, cm{} {
+    int seen[kBL + 1] = {};
     for (int c = 0; c <= kBL; ++c) {
       start[c] = class_start(kBL, c);
       size[c] = binom(kBL, c);
       screened[c] = i15_class(kBL, c);
     }
     start[kBL + 1] = 1 << kBL;
+    for (int s = 0; s < (1 << kBL); ++s) {
+      int c = 0;
+      for (int b = 0; b < kBL; ++b) c += (s >> b) & 1;
+      cm[s] = (unsigned short)(start[c] + seen[c]++);
+    }
   }
 };
 __constant__ BatchClassTab c_btab{};
@@ -64,13 +71,6 @@ __device__ inline void batch_group_prefix(const double* __restrict__ tab, double
     }
     batch_group_prefix<C + 1, SMALL_ONLY>(tab, gpre);
   }
-}
-
-// next integer with the same number of set bits (Gosper's hack; the division
-// by the lowest set bit c = v & -v is a shift by its position)
-__device__ __forceinline__ int next_same_popc(int v) {
-  const int c = v & -v, r = v + c;
-  return (int)((unsigned)(r ^ v) >> (1 + __ffs(v))) | r;
 }
 
 template <unsigned KIND>
@@ -118,12 +118,13 @@ k_exact_batch(const BatchOption* __restrict__ opts, BatchArgs ba, double2* __res
   // in the compare direction inside the class; ties by leaf index)
   constexpr int PER = (NL + kBThreads - 1) / kBThreads;  // positions per thread
   double v[PER];
-  int pos[PER];
+  int pos[PER], cmp[PER];
 #pragma unroll
   for (int q = 0; q < PER; ++q) {
     const int sfx = tid + kBThreads * q;
     v[q] = 0.0;
     pos[q] = -1;
+    cmp[q] = 0;
     if (TAB && sfx < NL) {
       double r = 1.0, c = 0.0, mx = 0.0, mn = INFINITY;
       for (int j = 0; j < kBL; ++j) {
@@ -133,7 +134,8 @@ k_exact_batch(const BatchOption* __restrict__ opts, BatchArgs ba, double2* __res
         mn = fmin(mn, r);
       }
       v[q] = (AC || AP) ? c : FL ? mx : mn;
-      tab[sfx] = v[q];
+      cmp[q] = c_btab.cm[sfx];
+      tab[cmp[q]] = v[q];  // staged class by class, leaf order inside a class
     }
   }
   __syncthreads();
@@ -142,13 +144,15 @@ k_exact_batch(const BatchOption* __restrict__ opts, BatchArgs ba, double2* __res
     const int sfx = tid + kBThreads * q;
     if (TAB && sfx < NL) {
       const int cls = __popc(sfx);
+      const int k0 = c_btab.start[cls], k1 = c_btab.start[cls + 1];
       int rank = 0;
-      // the class's leaves only: every cls-bit pattern below 2^kBL in order
-      for (int s2 = (1 << cls) - 1; s2 < NL; s2 = cls ? next_same_popc(s2) : NL) {
-        const double v2 = tab[s2];
-        rank += DESC ? (v2 > v[q] || (v2 == v[q] && s2 < sfx)) : (v2 < v[q] || (v2 == v[q] && s2 < sfx));
+      // the class's leaves only (a contiguous run of the staged table); ties
+      // by leaf index, which is the staged order
+      for (int k = k0; k < k1; ++k) {
+        const double v2 = tab[k];
+        rank += DESC ? (v2 > v[q] || (v2 == v[q] && k < cmp[q])) : (v2 < v[q] || (v2 == v[q] && k < cmp[q]));
       }
-      pos[q] = c_btab.start[cls] + rank;
+      pos[q] = k0 + rank;
     }
   }
   __syncthreads();
