@@ -25,9 +25,10 @@
 // mapping, so results do not depend on the grid, the GPU count or timing.
 //
 // Work items: (rep, stratum, chunk of kChunk draws).  A CTA evaluates one
-// item: thread t takes draws chunk_base + t + 256 k, keeps a Welford
-// (n, mean, M2), the CTA merges them with Chan's formula in a fixed tree,
-// and a second kernel merges the items of a stratum in ascending order.
+// item: thread t takes the pairs of draws chunk_base + 2 t + 512 k (+ 1) in
+// lock step, keeps shifted sums (n, mean, M2), the CTA merges them with
+// Chan's formula in a fixed tree, and a second kernel merges the items of a
+// stratum in ascending order.
 #include "bp_kernels.h"
 
 namespace bp {
