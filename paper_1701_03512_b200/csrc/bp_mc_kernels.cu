@@ -81,18 +81,6 @@ struct PathState {
   double S, sum, mx, mn;
 };
 
-__device__ __forceinline__ PathState prefix_state(const McArgs& a, unsigned long long m) {
-  PathState st{a.S0, 0.0, -INFINITY, INFINITY};
-  for (int t = 0; t < a.r; ++t) {
-    const int b = (int)((m >> (a.r - 1 - t)) & 1ull);
-    st.S *= b ? a.u : a.d;
-    st.sum += st.S;
-    st.mx = fmax(st.mx, st.S);
-    st.mn = fmin(st.mn, st.S);
-  }
-  return st;
-}
-
 __device__ __forceinline__ double payoff_of(unsigned kind, const PathState& st, double K, double invN) {
   const double mean = st.sum * invN;
   switch (kind) {
@@ -140,6 +128,37 @@ __device__ __forceinline__ void build_tables(const McArgs& a, McTables& t) {
     t.ec[b] = make_double2(r, c);
     t.xn[b] = make_double2(x, n);
   }
+}
+
+// State after the r prefix steps of stratum m (bit r - 1 of m is the first
+// step), through the step tables: whole bytes, a nibble, then single steps.
+__device__ __forceinline__ PathState prefix_state(const McArgs& a, const McTables& tab, unsigned long long m) {
+  PathState st{a.S0, 0.0, -INFINITY, INFINITY};
+  if (a.r == 0) return st;
+  const unsigned long long rev = __brevll(m) >> (64 - a.r);  // first step = bit 0, the tables' order
+  auto advance = [&](double e, double c, double x, double n) {
+    st.sum = fma(st.S, c, st.sum);
+    st.mx = fmax(st.mx, st.S * x);
+    st.mn = fmin(st.mn, st.S * n);
+    st.S *= e;
+  };
+  int t = 0;
+  for (; t + 8 <= a.r; t += 8) {
+    const int b = (int)((rev >> t) & 255ull);
+    advance(tab.ec[b].x, tab.ec[b].y, tab.xn[b].x, tab.xn[b].y);
+  }
+  if (t + 4 <= a.r) {
+    const Nib q = tab.nib[(rev >> t) & 15ull];
+    advance(q.e, q.c, q.x, q.n);
+    t += 4;
+  }
+  for (; t < a.r; ++t) {
+    st.S *= ((rev >> t) & 1ull) ? a.u : a.d;
+    st.sum += st.S;
+    st.mx = fmax(st.mx, st.S);
+    st.mn = fmin(st.mn, st.S);
+  }
+  return st;
 }
 
 constexpr uint32_t kMcPlaneBlocks = kMcLevels / 4;     // Philox blocks per group of 32 steps
@@ -266,20 +285,26 @@ __device__ __forceinline__ void walk_suffix_n(const McArgs& a, const McTables& t
   // whole bytes of 8 steps, one table entry each: entry address = table
   // base + 16 x byte (PRMT + LEA; tab_s is the table's shared-window address,
   // made once per kernel)
+  auto byte_step = [&](int g, int k) {
+#pragma unroll
+    for (int d = 0; d < NS; ++d) {
+      const uint32_t addr = tab_s + (__byte_perm(B[d][g], 0u, 0x4440u + k) << 4);
+      double e, c, x = 0.0, n = 0.0;
+      asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(e), "=d"(c) : "r"(addr));
+      if (need_max || need_min) asm("ld.shared.v2.f64 {%0, %1}, [%2+4096];" : "=d"(x), "=d"(n) : "r"(addr));
+      advance(s[d], e, c, x, n);
+    }
+  };
 #pragma unroll
   for (int g = 0; g < 2; ++g) {
+    const int cnt = nbytes - 4 * g;
+    if (cnt >= 4) {  // a whole group: no per-byte test
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      if (4 * g + k < nbytes) {
+      for (int k = 0; k < 4; ++k) byte_step(g, k);
+    } else {
 #pragma unroll
-        for (int d = 0; d < NS; ++d) {
-          const uint32_t addr = tab_s + (__byte_perm(B[d][g], 0u, 0x4440u + k) << 4);
-          double e, c, x = 0.0, n = 0.0;
-          asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(e), "=d"(c) : "r"(addr));
-          if (need_max || need_min) asm("ld.shared.v2.f64 {%0, %1}, [%2+4096];" : "=d"(x), "=d"(n) : "r"(addr));
-          advance(s[d], e, c, x, n);
-        }
-      }
+      for (int k = 0; k < 3; ++k)
+        if (k < cnt) byte_step(g, k);
     }
   }
   // a leftover nibble, then up to 3 single steps
@@ -357,7 +382,7 @@ k_mc_strata(const __grid_constant__ McArgs a, const unsigned long long* __restri
     const unsigned long long first = item_first[li];
     const unsigned long long R = draws[m];
     const unsigned long long last = first + kChunk < R ? first + kChunk : R;
-    const PathState pre = prefix_state(a, m);
+    const PathState pre = prefix_state(a, tab, m);
     ShiftedSums acc{0.0, 0.0, 0.0, 0.0};
     // whole pairs (2 j, 2 j + 1) in groups of kMcNS consecutive draws per
     // thread, then the remaining draws one per thread; an item starting at an
