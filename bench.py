@@ -482,7 +482,7 @@ def secondary_configs(dev):
                                   "philox_blocks_per_s": 4.5 * (R_m << k) / (t * 1e-3),
                                   "philox_ceiling_blocks_per_s": 5.15e11,
                                   "frac_of_philox_ceiling": 4.5 * (R_m << k) / (t * 1e-3) / 5.15e11,
-                                  "warp_inst_per_draw": 365.5,
+                                  "warp_inst_per_draw": 353.4,
                                   "note": "bit-sliced sampler: 8 threshold bits decided 32 steps per Philox word, "
                                           "tie words for the 2^-8 rest (exactly floor(p 2^32)/2^32 per step); "
                                           "ceiling = Philox4x32-10 alone, tools/microbench/mb_philox.cu "
