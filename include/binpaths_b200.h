@@ -158,9 +158,13 @@ int bp_exact_batch(const bp_tree* trees, int n_opts, uint32_t payoff,
 
 /* Stratified Monte Carlo statistics.  The first r steps of every draw of
  * stratum m are the r binary digits of m (step 1 = most significant); the
- * remaining N - r steps are Bernoulli(up_probs[t]) draws from
- * Philox4x32-10 with key = seed and counter = (word-block, draw, stratum,
- * rep).  For stratum m and repetition rep0 + k it writes the mean theta and
+ * remaining N - r steps are Bernoulli(floor(up_probs[t] 2^32) / 2^32) draws
+ * from Philox4x32-10 with key = seed and counter = (word-block, draw,
+ * stratum, rep); which word decides which step (32 steps per word, 8
+ * threshold bits, then tie words) is laid out in csrc/bp_mc_kernels.cu's
+ * header and restated step by step in oracle/bp_oracle.c (mc_suffix_bits).
+ * Results depend on (seed, stratum, rep, draw index) only, never on the
+ * grid, the device or the split into ranges.  For stratum m and repetition rep0 + k it writes the mean theta and
  * the sum of squared deviations sse of the draws[m] payoffs (undiscounted,
  * the theta scale of mc.py:197-213).  Strata with draws[m] == 0 report
  * (0, 0).  Outputs are [n_reps][2^r] arrays in host memory.            */
