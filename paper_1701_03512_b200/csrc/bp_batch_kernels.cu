@@ -147,11 +147,12 @@ k_exact_batch(const BatchOption* __restrict__ opts, BatchArgs ba, double2* __res
       const int k0 = c_btab.start[cls], k1 = c_btab.start[cls + 1];
       int rank = 0;
       // the class's leaves only (a contiguous run of the staged table); ties
-      // by leaf index, which is the staged order
-      for (int k = k0; k < k1; ++k) {
-        const double v2 = tab[k];
-        rank += DESC ? (v2 > v[q] || (v2 == v[q] && k < cmp[q])) : (v2 < v[q] || (v2 == v[q] && k < cmp[q]));
-      }
+      // go by leaf index, which is the staged order: an equal value ahead of
+      // this leaf counts, one behind it does not -- one compare per element
+#pragma unroll 4
+      for (int k = k0; k < cmp[q]; ++k) rank += DESC ? (tab[k] >= v[q]) : (tab[k] <= v[q]);
+#pragma unroll 4
+      for (int k = cmp[q] + 1; k < k1; ++k) rank += DESC ? (tab[k] > v[q]) : (tab[k] < v[q]);
       pos[q] = k0 + rank;
     }
   }
