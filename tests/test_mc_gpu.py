@@ -207,3 +207,37 @@ def test_sampler_later_ties_match_oracle_at_depth():
                                23, 2, 1)
     np.testing.assert_allclose(theta, ot, rtol=1e-12)
     np.testing.assert_allclose(sse, os_, rtol=1e-9)
+
+
+def test_forced_and_impossible_steps_in_the_suffix_match_oracle():
+    """Per-step probabilities with p = 1 (forced up, not drawn) and p = 0 steps
+    inside the stream-decided suffix, including the first suffix step, in both
+    32-step groups (N = 40, r = 2), and a constant-p tree whose first suffix
+    step is forced (the kernel then takes the general path)."""
+    N, r = 40, 2
+    rng = np.random.default_rng(12)
+    probs = rng.uniform(0.1, 0.9, size=N)
+    probs[[r, 7, 33, 39]] = 1.0
+    probs[[5, 20, 36]] = 0.0
+    inputs = bp.MarketInputs(S0=50.0, K=48.0, q=0.02, sigma=0.3, T=1.0, N=N)
+    base = bp.derive_crr(inputs)
+
+    def tree(p):  # with_custom_probs keeps to the open interval; the engine takes [0, 1]
+        return bp.TreeParams(dt=base.dt, u=base.u, d=base.d, beta=base.beta, up_probs=p)
+
+    params = tree(probs)
+    draws = [3000, 1, 4097, 500]
+    for tag in ("asian-call", "lookback-put"):
+        req = bp.ValuationRequest(inputs=inputs, params=params, kind=bp.resolve_kind(tag), force_large=True)
+        theta, sse, _ = bp.mc._strata_stats(req, r, draws, 31, 0, 2)
+        ot, os_ = oracle.mc_strata(N, 50.0, 48.0, params.u, params.d, params.up_probs, tag, r, draws, 31, 0, 2)
+        np.testing.assert_allclose(theta, ot, rtol=1e-12, atol=1e-12)
+        np.testing.assert_allclose(sse, os_, rtol=1e-9, atol=1e-9)
+    const = np.full(N, 0.55)
+    const[r] = 1.0
+    params = tree(const)
+    req = bp.ValuationRequest(inputs=inputs, params=params, kind=bp.ASIAN_CALL, force_large=True)
+    theta, sse, _ = bp.mc._strata_stats(req, r, draws, 32, 1, 1)
+    ot, os_ = oracle.mc_strata(N, 50.0, 48.0, params.u, params.d, params.up_probs, "asian-call", r, draws, 32, 1, 1)
+    np.testing.assert_allclose(theta, ot, rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(sse, os_, rtol=1e-9, atol=1e-9)
