@@ -460,6 +460,18 @@ def secondary_configs(dev):
     import paper_1701_03512_b200 as bp
     from paper_1701_03512_b200 import mc as bmc
     out = {}
+    # configs[0] (N = 20, the reference's own CPU-runnable case): launch-bound on a GPU
+    wl1, crr1 = workloads()
+    req1, kinds1, _ = make_req(wl1["config1"], crr1)
+    r1 = [bp.value_exact(req1, kinds=kinds1, devices=[dev]) for _ in range(8)]
+    t0 = time.perf_counter()
+    for _ in range(50):
+        bp.value_exact(req1, kinds=kinds1, devices=[dev])
+    call_s = (time.perf_counter() - t0) / 50
+    k1 = min(r.kernel_ms for r in r1[2:])
+    out["config1"] = {"workload": "exact Asian call, N=20 (2^20 paths): launch-bound on a GPU",
+                      "kernel_ms": k1, "call_ms": call_s * 1e3, "value": (1 << 20) / call_s, "unit": "paths/s",
+                      "asian_call": r1[-1].values["asian-call"]}
     N, k, R_m = 64, 12, 65536
     P = bp.classic_crr(N, 0.2, 0.05, 1.0)
     req = object.__new__(bp.ValuationRequest)
