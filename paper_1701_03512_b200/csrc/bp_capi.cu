@@ -1672,18 +1672,16 @@ static int mc_strata_ranges(const bp_tree* tree, uint32_t payoff, int r, const u
     if (draws[m] >= (1ull << 32)) return fail(BP_E_INVALID_INPUT, "at most 2^32 - 1 draws per stratum");
     if (first && first[m] > draws[m]) return fail(BP_E_INVALID_INPUT, "draw range with first > end");
   }
-  // work items of one repetition, stratum-ascending
+  // work items of one repetition, stratum-ascending: the host counts them per
+  // stratum, the device lists them (launch_mc_items)
   const unsigned long long CH = mc_chunk();
-  std::vector<unsigned long long> item_stratum, item_first, stratum_item0(M + 1, 0);
+  std::vector<unsigned long long> stratum_item0(M + 1, 0), first0(first ? M : 0);
   for (int m = 0; m < M; ++m) {
-    stratum_item0[m] = item_stratum.size();
-    for (unsigned long long f = first ? first[m] : 0; f < draws[m]; f += CH) {
-      item_stratum.push_back(m);
-      item_first.push_back(f);
-    }
+    const unsigned long long f = first ? first[m] : 0;
+    if (first) first0[m] = f;
+    stratum_item0[m + 1] = stratum_item0[m] + (draws[m] > f ? (draws[m] - f + CH - 1) / CH : 0);
   }
-  stratum_item0[M] = item_stratum.size();
-  const unsigned long long items_per_rep = item_stratum.size();
+  const unsigned long long items_per_rep = stratum_item0[M];
   BP_CUDA(cudaSetDevice(device));
   keep_pool(device);
   cudaStream_t st;
@@ -1709,14 +1707,15 @@ static int mc_strata_ranges(const bp_tree* tree, uint32_t payoff, int r, const u
   BP_CUDA(cudaMallocAsync((void**)&d_theta.p, sizeof(double) * (size_t)M * n_reps, st));
   BP_CUDA(cudaMallocAsync((void**)&d_sse.p, sizeof(double) * (size_t)M * n_reps, st));
   BP_CUDA(cudaMemcpyAsync(d_draws.p, draws, sizeof(unsigned long long) * M, cudaMemcpyHostToDevice, st));
-  if (items_per_rep) {
-    BP_CUDA(cudaMemcpyAsync(d_is.p, item_stratum.data(), sizeof(unsigned long long) * items_per_rep,
-                            cudaMemcpyHostToDevice, st));
-    BP_CUDA(cudaMemcpyAsync(d_if.p, item_first.data(), sizeof(unsigned long long) * items_per_rep,
-                            cudaMemcpyHostToDevice, st));
-  }
   BP_CUDA(cudaMemcpyAsync(d_i0.p, stratum_item0.data(), sizeof(unsigned long long) * (M + 1),
                           cudaMemcpyHostToDevice, st));
+  DevBuf<unsigned long long> d_first;
+  d_first.st = st;
+  if (first) {
+    BP_CUDA(cudaMallocAsync((void**)&d_first.p, sizeof(unsigned long long) * M, st));
+    BP_CUDA(cudaMemcpyAsync(d_first.p, first0.data(), sizeof(unsigned long long) * M, cudaMemcpyHostToDevice, st));
+  }
+  BP_CUDA(launch_mc_items(d_draws.p, d_first.p, d_i0.p, M, d_is.p, d_if.p, st));
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);

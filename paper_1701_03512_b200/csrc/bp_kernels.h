@@ -60,6 +60,10 @@ struct McArgs {
   uint32_t rk[20];  // Philox round keys of (key0, key1)
   uint32_t rep0;
 };
+// item lists of one repetition: stratum m's chunks of mc_chunk() draws from first[m] (nullptr: 0) to draws[m]
+cudaError_t launch_mc_items(const unsigned long long* draws_dev, const unsigned long long* first_dev,
+                            const unsigned long long* stratum_item0_dev, int n_strata,
+                            unsigned long long* item_stratum_dev, unsigned long long* item_first_dev, cudaStream_t st);
 cudaError_t launch_mc_strata(const McArgs& a, const unsigned long long* draws_dev,
                              const unsigned long long* item_stratum_dev, const unsigned long long* item_first_dev,
                              unsigned long long items_per_rep, int n_reps, int n_strata, double* item_out_dev,

@@ -432,6 +432,28 @@ __global__ void k_mc_strata_merge(const double* __restrict__ item_out, const uns
   sse[idx] = acc.n > 0.0 ? acc.m2 : 0.0;
 }
 
+// item -> (stratum, first draw) lists, one thread per stratum
+__global__ void k_mc_items(const unsigned long long* __restrict__ draws, const unsigned long long* __restrict__ first,
+                           const unsigned long long* __restrict__ stratum_item0, int n_strata,
+                           unsigned long long* __restrict__ item_stratum, unsigned long long* __restrict__ item_first) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= n_strata) return;
+  unsigned long long it = stratum_item0[m];
+  for (unsigned long long f = first ? first[m] : 0ull; f < draws[m]; f += kChunk, ++it) {
+    item_stratum[it] = (unsigned long long)m;
+    item_first[it] = f;
+  }
+}
+
+cudaError_t launch_mc_items(const unsigned long long* draws_dev, const unsigned long long* first_dev,
+                            const unsigned long long* stratum_item0_dev, int n_strata,
+                            unsigned long long* item_stratum_dev, unsigned long long* item_first_dev,
+                            cudaStream_t st) {
+  k_mc_items<<<(n_strata + 127) / 128, 128, 0, st>>>(draws_dev, first_dev, stratum_item0_dev, n_strata,
+                                                     item_stratum_dev, item_first_dev);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_mc_strata(const McArgs& a, const unsigned long long* draws_dev,
                              const unsigned long long* item_stratum_dev, const unsigned long long* item_first_dev,
                              unsigned long long items_per_rep, int n_reps, int n_strata, double* item_out_dev,
