@@ -190,16 +190,42 @@ def _tree(req):
     return tree_of(req)
 
 
+_PARTITIONS: dict = {}  # (n, M) -> the canonical prefix partition (immutable; a few entries)
+_MASSES: dict = {}      # (n, M, prefix probabilities) -> stratum masses of that partition
+
+
 def _stratified_partition(req, M: int) -> PathPartition:
     if M & (M - 1) != 0:
         raise InvalidWorkerCount(f"stratum count must be a power of two, got {M}")
     n = int(req.inputs.N)
+    hit = _PARTITIONS.get((n, M))
+    if hit is not None:
+        return hit
     if n > 62:  # MC only: 63/64-step paths (BASELINE config 4), prefix strata as in make_partition
         r = M.bit_length() - 1
         if r > n:
             raise InvalidWorkerCount(f"stratum count {M} exceeds the paths of an {n}-step tree")
-        return PathPartition(n=n, m=M, prefix_width=r, blocks=tuple((i,) for i in range(M)))
-    return make_partition(n, M)
+        part = PathPartition(n=n, m=M, prefix_width=r, blocks=tuple((i,) for i in range(M)))
+    else:
+        part = make_partition(n, M)
+    if len(_PARTITIONS) >= 8:
+        _PARTITIONS.clear()
+    _PARTITIONS[(n, M)] = part
+    return part
+
+
+def _stratum_masses(req, part: PathPartition) -> list:
+    """partition_masses of a _stratified_partition, remembered per lattice
+    prefix (repeated estimates on one tree: 4096 strata cost ~2 ms in Python)."""
+    probs = np.asarray(req.params.up_probs, dtype=np.float64)
+    key = (part.n, part.m, probs[:part.prefix_width].tobytes(), probs.shape[0])
+    hit = _MASSES.get(key)
+    if hit is None:
+        hit = partition_masses(req.params, part)
+        if len(_MASSES) >= 8:
+            _MASSES.clear()
+        _MASSES[key] = hit
+    return hit
 
 
 def _strata_stats(req, r: int, draws, seed: int, rep0: int, n_reps: int):
@@ -260,7 +286,7 @@ def _partitioned_from(req, cfg, masses, alloc, thetas, sses, equal: bool) -> Est
     variance = disc * disc * var_theta
     return Estimate(value=disc * float(np.sum(th * w)), variance=variance, std_error=math.sqrt(variance),
                     R_used=int(sum(alloc)), method="partitioned", seed=cfg.seed,
-                    per_stratum=tuple((m, int(alloc[m]), float(th[m])) for m in range(len(alloc))))
+                    per_stratum=tuple(zip(range(len(alloc)), map(int, alloc), th.tolist())))
 
 
 def _basic_reps(req, cfg, rep0, n_reps, stats=None):
@@ -274,7 +300,7 @@ def _partitioned_reps(req, cfg, rep0, n_reps, stats=None):
     if cfg.R < cfg.M:
         raise InfeasibleAllocation(f"partitioned estimator needs R >= M, got R={cfg.R}, M={cfg.M}")
     part = _stratified_partition(req, cfg.M)
-    masses = partition_masses(req.params, part)
+    masses = _stratum_masses(req, part)
     alloc = allocate_strata(part, req.params, cfg.R)
     theta, sse, _ = (stats or _strata_stats)(req, part.prefix_width, alloc, cfg.seed, rep0, n_reps)
     return [_partitioned_from(req, cfg, masses, alloc, theta[k], sse[k], equal=False) for k in range(n_reps)]
@@ -282,7 +308,7 @@ def _partitioned_reps(req, cfg, rep0, n_reps, stats=None):
 
 def _equal_reps(req, cfg, rep0, n_reps, stats=None):
     part = _stratified_partition(req, cfg.M)
-    masses = partition_masses(req.params, part)
+    masses = _stratum_masses(req, part)
     alloc = [cfg.R] * cfg.M
     theta, sse, _ = (stats or _strata_stats)(req, part.prefix_width, alloc, cfg.seed, rep0, n_reps)
     return [_partitioned_from(req, cfg, masses, alloc, theta[k], sse[k], equal=True) for k in range(n_reps)]
@@ -292,7 +318,7 @@ def _shared_reps(req, cfg, rep0, n_reps):
     if cfg.R < 2:
         raise InvalidInput(f"shared estimator needs R >= 2, got {cfg.R}")
     part = _stratified_partition(req, cfg.M)
-    masses = np.array(partition_masses(req.params, part))
+    masses = np.array(_stratum_masses(req, part))
     tree, keep = _tree(req)
     im = np.zeros(n_reps)
     isse = np.zeros(n_reps)
@@ -310,7 +336,7 @@ def _shared_reps(req, cfg, rep0, n_reps):
         variance = disc * disc * (float(isse[k]) / (cfg.R * cfg.R))
         out.append(Estimate(value=disc * float(im[k]), variance=variance, std_error=math.sqrt(variance),
                             R_used=cfg.R, method="shared", seed=cfg.seed,
-                            per_stratum=tuple((m, cfg.R, float(sm[k, m])) for m in range(cfg.M))))
+                            per_stratum=tuple(zip(range(cfg.M), [cfg.R] * cfg.M, sm[k].tolist()))))
     return out
 
 
