@@ -189,6 +189,11 @@ def value_leaf_formula(req) -> float:
     return math.exp(-req.inputs.q * req.inputs.T) * float(np.dot(weights, values))
 
 
+_BP_TREE_DTYPE = np.dtype([(name, {ctypes.c_int32: "<i4", ctypes.c_double: "<f8", ctypes.c_void_p: "<u8"}[ct])
+                           for name, ct in _native.BpTree._fields_], align=True)
+assert _BP_TREE_DTYPE.itemsize == ctypes.sizeof(_native.BpTree)
+
+
 def price_batch(N: int, S0, K, u, d, p, disc, kind, device: int = 0, with_time: bool = False):
     """Exact values of many independent trees (arrays, same N), one kind,
     one launch (bp_exact_batch).  Returns a numpy array (and kernel ms)."""
@@ -196,9 +201,13 @@ def price_batch(N: int, S0, K, u, d, p, disc, kind, device: int = 0, with_time: 
     n = arrs[0].size
     S0a, Ka, ua, da, pa, da_ = (np.ascontiguousarray(a.reshape(-1)) for a in arrs)
     probs = np.ascontiguousarray(np.repeat(pa[:, None], N, axis=1))
-    trees = (_native.BpTree * n)()
-    for i in range(n):
-        trees[i] = _native.BpTree(int(N), 0, S0a[i], Ka[i], ua[i], da[i], da_[i], probs[i].ctypes.data)
+    # the bp_tree array, filled column by column through a structured view of the same layout
+    rec = np.zeros(n, dtype=_BP_TREE_DTYPE)
+    rec["n_steps"] = int(N)
+    for name, col in (("S0", S0a), ("K", Ka), ("u", ua), ("d", da), ("disc", da_)):
+        rec[name] = col
+    rec["up_probs"] = probs.ctypes.data + np.arange(n, dtype=np.uint64) * np.uint64(8 * int(N))
+    trees = ctypes.cast(rec.ctypes.data, ctypes.POINTER(_native.BpTree))
     out = np.zeros(n)
     ms = ctypes.c_double()
     _native.check(_native.lib().bp_exact_batch(trees, n, 1 << kind_bit(kind), int(device), _native.dptr(out),

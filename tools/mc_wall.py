@@ -21,3 +21,16 @@ ts = []
 for i in range(5):
     t0 = time.perf_counter(); e = bp.estimate_partitioned_equal(req, bp.McConfig(R=R_m, M=1 << k, seed=0)); ts.append((time.perf_counter() - t0) * 1e3)
 print("estimate_partitioned_equal wall min %.3f ms" % min(ts))
+# config 5: the batched exact call
+import math
+n, Nb = 4096, 24
+rng = np.random.default_rng(0)
+S0 = rng.uniform(50, 150, n); m = rng.uniform(0.8, 1.2, n); K = m * S0
+sigma = rng.uniform(0.1, 0.5, n); r = rng.uniform(0.0, 0.08, n); T = rng.uniform(0.25, 3.0, n)
+u = np.exp(sigma * np.sqrt(T / Nb)); d = 1.0 / u
+p = (np.exp(r * T / Nb) - d) / (u - d); disc = np.exp(-r * T)
+for i in range(2): bp.price_batch(Nb, S0, K, u, d, p, disc, bp.ASIAN_CALL, device=0, with_time=True)
+ts = []
+for i in range(5):
+    t0 = time.perf_counter(); vals, kms = bp.price_batch(Nb, S0, K, u, d, p, disc, bp.ASIAN_CALL, device=0, with_time=True); ts.append((time.perf_counter() - t0) * 1e3)
+print("price_batch wall min %.3f ms, kernel %.3f ms" % (min(ts), kms))
